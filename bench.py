@@ -1,0 +1,377 @@
+#!/usr/bin/env python3
+"""bench.py -- exact-match queries/s on B200 (arXiv 1303.3692's hot path), one JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...          (one rank per GPU, NCCL)
+
+A step is one pass of the hot path -- ``sa_match_batch`` over this rank's whole batch of packed
+reads (bracket lookup, joint lo/hi binary search, interval write) -- with the index and the reads
+already resident in HBM.  The index build is off the timed path.
+Multi-GPU: the index is replicated, every rank matches its own fixed-size shard of reads (weak
+scaling, no data-path collective); elapsed time is the max over ranks (NCCL all_reduce MAX).
+
+`--impl reference` times the CPU oracle (oracle/: the streaming counting oracle, no suffix array)
+on a bounded sample of the same workload on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "exact-match queries/sec and achieved HBM GB/s at 1/2/4/8 B200"
+UNIT = "queries/s"
+
+
+def log(*a):
+    if int(os.environ.get("RANK", "0")) == 0:
+        print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--m", type=int, default=None, help="C5 read length (16..1000)")
+    ap.add_argument("--q", type=int, default=None, help="override reads per GPU")
+    ap.add_argument("--k", type=int, default=0, help="k-mer bracket k (0 = auto)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def workload(args):
+    cfg = synth.CONFIGS[args.config]
+    if args.config == "C5":
+        cfg = cfg.with_m(args.m or 100)
+    if args.q:
+        cfg = synth.Config(cfg.name, cfg.ref_kind, cfg.n, cfg.ref_seed, args.q, cfg.m_min, cfg.m_max, cfg.p_random,
+                           cfg.p_mut_read, cfg.read_seed, cfg.description)
+    return cfg
+
+
+def config_json(cfg, world, k=None):
+    d = {"workload": f"{cfg.name}: {cfg.description}", "n_bases": cfg.n, "reads_per_gpu": cfg.Q,
+         "global_reads": cfg.Q * world, "read_len": (cfg.m_min if cfg.m_min == cfg.m_max else [cfg.m_min, cfg.m_max]),
+         "parallelism": f"replicated index x{world}, read shards (no data-path collective)",
+         "l2": "inputs larger than L2 (index + reads >> 126 MB); no flush" if cfg.n * 4 > 2 ** 30 else
+               "index fits L2 (L2-resident workload); no flush"}
+    if k is not None:
+        d["kmer_k"] = k
+    return d
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            log("NVML unavailable:", e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def result(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": rs,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes_per_query(n, k, m):
+    """sector-granular bytes the k-mer-bracket joint search must move per query.
+
+    1 table sector (32 B) + D steps x (SA sector + text sector, 32 B each) + the packed read (m/4 B,
+    streamed) + the {lo, hi} result (8 B); D = log2(mean bracket + 1) + 1 (the joint lo/hi search:
+    one descent plus on average one extra level for the hi continuation)."""
+    bracket = n / float(4 ** k)
+    D = math.log2(bracket + 1.0) + 1.0
+    return 32.0 + D * 64.0 + math.ceil(m / 4.0) + 8.0
+
+
+def traffic_per_launch(workload_name):
+    """dram bytes (read + write) per k_match launch from the committed ncu --set full summary, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(workload_name)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference_arm(args):
+    """The CPU oracle on this box's host cores (rank 0 only)."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = workload(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    t0 = time.time()
+    ref = cfg.reference()
+    S = oracle.encode(ref)
+    log(f"reference generated+encoded in {time.time() - t0:.1f}s")
+    cores = oracle.max_threads()
+    s = sample_size(cfg, cores, args.cpu_seconds)
+    times = []
+    for it in range(args.warmup + args.steps):
+        # each step: a fresh bounded sample of the same read stream
+        words, lens = cfg.reads(ref, q_begin=it * s, q_count=s)
+        t = time.perf_counter()
+        oracle.count_batch(S, words, lens)
+        dt = time.perf_counter() - t
+        if it >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    v = s * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": config_json(cfg, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{s} reads per step of the {cfg.name} read stream, streaming counting "
+                                       f"oracle over all {cfg.n} suffixes (no suffix array)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def sample_size(cfg, cores, seconds):
+    """Reads per oracle sample so that one streaming pass costs ~`seconds` on `cores` threads.
+    Cost model: n * log2(2s) suffix-vs-key compares at ~6 ns each (measured on the dev box)."""
+    per_pass = cfg.n * 6e-9 / max(1, cores)
+    if per_pass <= 0:
+        return 64
+    lg = max(1.0, seconds / per_pass)
+    s = int(min(2 ** min(lg, 20) / 2, 1 << 16))
+    return max(16, min(s, cfg.Q))
+
+
+def cpu_baseline(cfg, ref, seconds):
+    import oracle
+    S = oracle.encode(ref)
+    cores = oracle.max_threads()
+    s = sample_size(cfg, cores, seconds)
+    words, lens = cfg.reads(ref, q_count=s)
+    t = time.perf_counter()
+    oracle.count_batch(S, words, lens)
+    dt = time.perf_counter() - t
+    return {"value": s / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "seconds": dt,
+            "sample": f"first {s} reads of the {cfg.name} read stream, streaming counting oracle over all "
+                      f"{cfg.n} suffixes (no suffix array), {cores} threads"}
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_1303_3692_b200 as sa
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = workload(args)
+
+    # ---- inputs + index (untimed) ----
+    t0 = time.time()
+    ref = cfg.reference()
+    log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
+    t0 = time.time()
+    idx = sa.Index(ref, k=args.k, device=local)
+    torch.cuda.synchronize()
+    log(f"index built in {time.time() - t0:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
+    t0 = time.time()
+    Q = cfg.Q
+    stride = cfg.stride
+    fixed = cfg.m_max if cfg.m_min == cfg.m_max else None
+    words_h = torch.empty((Q, stride), dtype=torch.int64, pin_memory=True)
+    lens_h = torch.empty(Q, dtype=torch.int32, pin_memory=True)
+    cfg.reads(ref, q_begin=rank * Q, words_out=words_h.numpy().view(np.uint64),
+              lens_out=lens_h.numpy().view(np.uint32))
+    words = words_h.to(dev, non_blocking=True)
+    lens = None if fixed else lens_h.to(dev, non_blocking=True)
+    out = torch.empty((Q, 2), dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+    log(f"{Q} reads/rank generated + uploaded in {time.time() - t0:.1f}s")
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    launch_ms = [a.elapsed_time(b) for a, b in ev]
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+
+    # per-shard summary gathered over NCCL (the only collective): hits, sum of counts, checksum
+    res = out.view(torch.int64)  # (lo | hi<<32) per read, for a cheap checksum
+    lo = out[:, 0].to(torch.int64) & 0xFFFFFFFF
+    hi = out[:, 1].to(torch.int64) & 0xFFFFFFFF
+    summary = torch.stack([(hi > lo).sum(), (hi - lo).sum(), (res * 0x9E3779B1).sum()]).to(torch.int64)
+    if world > 1:
+        allsum = [torch.empty_like(summary) for _ in range(world)]
+        dist.all_gather(allsum, summary)
+        summary_all = torch.stack(allsum).cpu().tolist()
+    else:
+        summary_all = [summary.cpu().tolist()]
+
+    total_reads = Q * world * args.steps
+    value = total_reads / (elapsed_ms * 1e-3)
+    ms_per_step = elapsed_ms / args.steps
+
+    # ---- roofline of the dominant (only) kernel: k_match ----
+    m_alg = cfg.m_max if fixed else (cfg.m_min + cfg.m_max) / 2
+    bpq = algorithmic_bytes_per_query(cfg.n, idx.k, m_alg)
+    avg_launch_s = statistics.mean(launch_ms) * 1e-3
+    achieved = bpq * Q / avg_launch_s / 1e9
+    peak, peak_src = measured_peaks()
+    traffic = traffic_per_launch(cfg.name)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_match", "algorithmic_bytes_per_query": bpq,
+                "peak_source": peak_src}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
+            "roofline": roofline, "clocks": sampler.result(), "gpu_launches": args.steps,
+            "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
+            "shards": summary_all}
+
+    # ---- random-gather microbenchmark (context for the roofline; untimed) ----
+    if rank == 0:
+        try:
+            rg = sa.random_gather(local, buffer_bytes=16 << 30, access_bytes=32, n_threads=148 * 2048 * 2, loads=64)
+            line["random_gather_32B"] = {"GBps": rg["GBps"], "Gsectors_per_s": rg["Gaccess_per_s"],
+                                         "note": "independent random 32-B loads over 16 GiB"}
+        except Exception as e:
+            line["random_gather_32B"] = {"error": str(e)}
+
+    # ---- e2e: the same match through the C ABI with HOST buffers (copies inside the timed region) ----
+    if not args.no_e2e:
+        out_h = torch.empty((Q, 2), dtype=torch.int32, pin_memory=True)
+        wn = words_h.numpy()
+        ln = None if fixed else lens_h.numpy()
+        on = out_h.numpy()
+        idx.match_host(wn, ln, fixed_len=fixed, out=on)  # warm-up (allocates staging)
+        e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(e2e_steps):
+            idx.match_host(wn, ln, fixed_len=fixed, out=on)
+        dt = time.perf_counter() - t
+        if world > 1:
+            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        if not np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32)):
+            raise RuntimeError("host-buffer path disagrees with the device path")
+        line["e2e"] = {"value": Q * world * e2e_steps / dt, "unit": UNIT,
+                       "h2d_bytes_per_step": Q * stride * 8 + (0 if fixed else Q * 4),
+                       "d2h_bytes_per_step": Q * 8, "steps": e2e_steps}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, ref, args.cpu_seconds)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    idx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * sa.h -- C ABI of libsa: batched exact matching of short reads against one
+ * reference genome by binary search over its suffix array, on NVIDIA B200
+ * (sm_100a).  The data-parallel hot path of arXiv 1303.3692 (PAPER.md,
+ * cited "P:L<line>"), re-designed for B200.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - Return codes only; no exceptions cross the ABI.  On failure a one-line
+ *    detail (e.g. the symbol and its position) is available from
+ *    sa_last_error() on the calling thread.
+ *  - "dev" pointers are CUDA device pointers on the index's device (e.g.
+ *    torch.Tensor.data_ptr()); "host" pointers are CPU memory (page-locked
+ *    memory is recommended where stated).  The caller owns every buffer it
+ *    passes; the library never frees them and keeps no reference after the
+ *    call's stream work completes.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default
+ *    stream).  Device-side calls are stream-ordered and asynchronous: results
+ *    are valid after the stream is synchronised.
+ *  - The index is immutable after sa_index_create; concurrent sa_match_batch /
+ *    sa_locate calls on different streams are safe.  sa_match_batch_host
+ *    serialises on an internal per-index lock.
+ *
+ * Alphabet and packing
+ * --------------------
+ *  Sigma = {a,c,g,t} ordered a<c<g<t (Sec. III), codes A=0 C=1 G=2
+ *  T=3.  A query of m bases is packed 2 bits per base, MSB-first, into uint64
+ *  words: base j of query q is at word q*stride_words + j/32, bits
+ *  [63-2(j%32) .. 62-2(j%32)].  Bits past m are ignored.
+ *
+ * What a match computes (Sec. IV; Alg. 1)
+ * ----------------------------------------------------------------
+ *  With SA the suffix array of S (Table I: all suffix starts in
+ *  lexicographic order, a proper prefix sorting first, no sentinel) and
+ *  t_i = S[i .. min(i+m, n)) the m-truncated suffix,
+ *      lo = #{ i : t_i <  P },   hi = #{ i : t_i <= P }.
+ *  [lo, hi) is the paper's [LB, RB] as a half-open interval: count = hi-lo,
+ *  positions = SA[lo..hi) in SA order ("namely 9, 0, 5").  A query that
+ *  does not occur ("(LB,RB) is NULL") yields lo == hi == its insertion
+ *  point.  m = 0 yields [0, n).  Results are unique, hence bit-exact.
+ */
+#ifndef SA_H
+#define SA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sa_index sa_index; /* opaque; owns all index memory on its device */
+
+typedef enum {
+    SA_OK = 0,
+    SA_EINVAL = -1,   /* bad argument: NULL pointer with Q > 0, stride < ceil(m/32), k out of range, ... */
+    SA_ESYMBOL = -2,  /* reference byte not in {A,C,G,T,a,c,g,t}; position in sa_last_error() */
+    SA_ETOOLONG = -3, /* n > 2^32 - 1 (the suffix array holds uint32 positions) */
+    SA_ENOMEM = -4,   /* device allocation failed */
+    SA_ECUDA = -5,    /* any other CUDA error, including "no device" */
+    SA_EEMPTY = -6    /* n == 0 */
+} sa_status;
+
+typedef struct {
+    int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device */
+    uint32_t kmer_k;   /* k of the k-mer bracket table, 1..16; 0 = auto (min(12, floor(log4 n))) */
+    uint32_t flags;    /* reserved, must be 0 */
+    uint32_t reserved; /* must be 0 */
+} sa_index_opts;
+
+/* Build the index of ref_ascii[0..n) (host memory, case-insensitive ACGT) on
+ * the device: validate + pack to 2 bits/base, build the suffix array on the
+ * GPU (radix sort + prefix doubling), build the k-mer bracket table.
+ * The index build is P:L105-150 (Sec. III) re-designed; it is not
+ * on the timed path.  opts may be NULL (defaults).  Synchronous.
+ * Errors: SA_EINVAL (ref_ascii or out NULL, bad opts), SA_EEMPTY (n == 0),
+ * SA_ETOOLONG, SA_ESYMBOL (first bad position reported), SA_ENOMEM, SA_ECUDA.
+ * On error *out is set to NULL and nothing is leaked. */
+sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa_index_opts *opts, sa_index **out);
+
+/* Free all device memory of the index.  NULL-safe.  Synchronises its device. */
+void sa_index_destroy(sa_index *idx);
+
+/* Any output pointer may be NULL.  device_bytes = resident index bytes. */
+sa_status sa_index_info(const sa_index *idx, uint64_t *n, uint32_t *kmer_k, uint64_t *device_bytes, int32_t *device);
+
+/* Copy the suffix array (n uint32, host) -- for checking it against the oracle. */
+sa_status sa_index_export_sa(const sa_index *idx, uint32_t *host_out);
+
+/* Copy the k-mer bracket table T (4^k + 1 uint32, host):
+ * T[x] = #{ i : trunc_k(S_i) < x } for x in [0, 4^k], x read as a k-mer. */
+sa_status sa_index_export_table(const sa_index *idx, uint32_t *host_out);
+
+/* Copy the packed text (ceil(n/32) words, host, same packing as queries). */
+sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
+
+/* Match Q packed queries (the hot path).
+ *   q_words   dev, Q*stride_words uint64, layout above.
+ *   q_len     dev, Q uint32 lengths, or NULL: every query has fixed_len bases.
+ *   out_lohi  dev, 2Q uint32: out_lohi[2q] = lo, out_lohi[2q+1] = hi
+ *             (Alg. 1 lines 44-45, res[thd<<1] = LB, res[(thd<<1)+1] = RB, reading A8).
+ *   workspace dev scratch of sa_match_workspace_size() bytes (may be NULL if that is 0).
+ *   flags     0 (reserved).
+ * Requirements: every length m <= 32*stride_words and m <= 65535.  Q == 0 is a
+ * no-op.  Errors: SA_EINVAL.  Asynchronous on `stream`. */
+sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, size_t *bytes);
+sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                         uint32_t stride_words, uint64_t Q, uint32_t *out_lohi, void *workspace, size_t ws_bytes,
+                         uint32_t flags, void *stream);
+
+/* The same match with HOST buffers (page-locked recommended): the queries are
+ * streamed host->device in chunks of chunk_Q queries (0 = auto), matched, and
+ * the intervals streamed back, with copies and kernels overlapped on internal
+ * streams.  Synchronous: out_lohi (host, 2Q uint32) is complete on return. */
+sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                              uint32_t stride_words, uint64_t Q, uint32_t *out_lohi, uint64_t chunk_Q);
+
+/* Locate (positions SA[lo..hi) per query, in SA order):
+ *   sa_locate_offsets: offsets (dev, Q+1 uint64) = exclusive prefix sum of hi-lo;
+ *                      offsets[Q] = total number of positions.
+ *   sa_locate:         positions (dev, offsets[Q] uint32): positions[offsets[q] + j] = SA[lo_q + j]. */
+sa_status sa_locate_workspace_size(uint64_t Q, size_t *bytes);
+sa_status sa_locate_offsets(const sa_index *idx, const uint32_t *out_lohi, uint64_t Q, uint64_t *offsets,
+                            void *workspace, size_t ws_bytes, void *stream);
+sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_t *offsets, uint64_t Q,
+                    uint32_t *positions, void *stream);
+
+/* Measurement tool (not on the path): random-access gather rate of the
+ * device's memory.  Allocates buffer_bytes, then every thread issues `loads`
+ * independent (dependent=0) or pointer-chased (dependent=1) loads of
+ * access_bytes (4, 8, 16 or 32) at hashed, access_bytes-aligned offsets.
+ * *ms = device time of one launch of n_threads threads (CUDA events). */
+sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,
+                                uint32_t loads, int32_t dependent, float *ms);
+
+/* Thread-local detail of the last failure on this thread ("" if none). */
+const char *sa_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t sa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SA_H */

@@ -1,0 +1,217 @@
+"""paper_1303_3692_b200 -- B200-native suffix-array exact matching (arXiv 1303.3692's hot path).
+
+A thin ctypes binding over the C ABI in ``include/sa.h`` (``libsa.so``, built in-tree by
+``make``).  The binding only marshals arguments: every step of the path (pack, suffix-array
+build, bracket table, search, locate) runs in the library's CUDA kernels.  PyTorch is used for
+device memory and streams.  There is no CPU fallback: if ``libsa.so`` is missing or no CUDA
+device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+__all__ = ["SAError", "Index", "lib", "random_gather", "LIB_PATH", "EXPORTED_SYMBOLS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsa.so")
+
+SA_OK, SA_EINVAL, SA_ESYMBOL, SA_ETOOLONG, SA_ENOMEM, SA_ECUDA, SA_EEMPTY = 0, -1, -2, -3, -4, -5, -6
+_NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
+          -6: "SA_EEMPTY"}
+
+_p, _u64, _u32, _i32, _sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_size_t
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("kmer_k", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
+
+
+# name -> (argtypes, restype); mirrors include/sa.h
+_SIGS = {
+    "sa_index_create": ([_p, _u64, ctypes.POINTER(_Opts), ctypes.POINTER(_p)], ctypes.c_int),
+    "sa_index_destroy": ([_p], None),
+    "sa_index_info": ([_p, ctypes.POINTER(_u64), ctypes.POINTER(_u32), ctypes.POINTER(_u64), ctypes.POINTER(_i32)],
+                      ctypes.c_int),
+    "sa_index_export_sa": ([_p, _p], ctypes.c_int),
+    "sa_index_export_table": ([_p, _p], ctypes.c_int),
+    "sa_index_export_text": ([_p, _p], ctypes.c_int),
+    "sa_match_workspace_size": ([_p, _u64, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
+    "sa_match_batch": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _sz, _u32, _p], ctypes.c_int),
+    "sa_match_batch_host": ([_p, _p, _p, _u32, _u32, _u64, _p, _u64], ctypes.c_int),
+    "sa_locate_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
+    "sa_locate_offsets": ([_p, _p, _u64, _p, _p, _sz, _p], ctypes.c_int),
+    "sa_locate": ([_p, _p, _p, _u64, _p, _p], ctypes.c_int),
+    "sa_tool_random_gather": ([_i32, _u64, _u32, _u64, _u32, _i32, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+    "sa_last_error": ([], ctypes.c_char_p),
+    "sa_version": ([], ctypes.c_int32),
+}
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """Load libsa.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `make` or __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+class SAError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        detail = lib().sa_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {_NAMES.get(code, code)}: {detail}")
+        self.code = code
+        self.detail = detail
+
+
+def _check(code: int, where: str):
+    if code != SA_OK:
+        raise SAError(code, where)
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream or None
+
+
+def _dptr(t) -> Optional[int]:
+    return None if t is None else (t.data_ptr() or None)
+
+
+class Index:
+    """Suffix-array index of one reference on one GPU (``sa_index_create``).
+
+    ref: str / bytes / numpy uint8 array of ACGT (case-insensitive).  k: bracket-table k (0 = auto).
+    """
+
+    def __init__(self, ref, k: int = 0, device: Optional[int] = None):
+        if isinstance(ref, str):
+            ref = ref.encode("ascii")
+        arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
+            np.ascontiguousarray(ref, dtype=np.uint8)
+        opts = _Opts(-1 if device is None else int(device), int(k), 0, 0)
+        h = _p()
+        _check(lib().sa_index_create(arr.ctypes.data if arr.size else None, arr.size, ctypes.byref(opts),
+                                     ctypes.byref(h)), "sa_index_create")
+        self._h = h
+        n, kk, nb, dev = _u64(), _u32(), _u64(), _i32()
+        _check(lib().sa_index_info(h, ctypes.byref(n), ctypes.byref(kk), ctypes.byref(nb), ctypes.byref(dev)),
+               "sa_index_info")
+        self.n, self.k, self.device_bytes, self.device = n.value, kk.value, nb.value, dev.value
+
+    # ---- lifetime ----
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sa_index_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- exports (for checking against the oracle) ----
+    def export_sa(self) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.uint32)
+        _check(lib().sa_index_export_sa(self._h, out.ctypes.data), "sa_index_export_sa")
+        return out
+
+    def export_table(self) -> np.ndarray:
+        out = np.empty((1 << (2 * self.k)) + 1, dtype=np.uint32)
+        _check(lib().sa_index_export_table(self._h, out.ctypes.data), "sa_index_export_table")
+        return out
+
+    def export_text(self) -> np.ndarray:
+        out = np.empty((self.n + 31) // 32, dtype=np.uint64)
+        _check(lib().sa_index_export_text(self._h, out.ctypes.data), "sa_index_export_text")
+        return out
+
+    # ---- the hot path ----
+    def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None):
+        """sa_match_batch on device tensors.
+
+        words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
+        lens:  CUDA int32 tensor [Q] (uint32 lengths) or None with fixed_len.
+        Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi); view it as uint32 on the host.
+        """
+        import torch
+        assert words.is_cuda and words.dtype == torch.int64 and words.dim() == 2 and words.is_contiguous()
+        Q, stride = words.shape
+        if lens is None and fixed_len is None:
+            raise ValueError("give lens or fixed_len")
+        if lens is not None:
+            assert lens.is_cuda and lens.dtype == torch.int32 and lens.numel() == Q and lens.is_contiguous()
+        if out is None:
+            out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
+        assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
+        _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(out),
+                                    None, 0, 0, _stream_ptr(stream)), "sa_match_batch")
+        return out
+
+    def match_host(self, words: np.ndarray, lens: Optional[np.ndarray] = None, fixed_len: Optional[int] = None,
+                   out: Optional[np.ndarray] = None, chunk: int = 0) -> np.ndarray:
+        """sa_match_batch_host: host buffers in (pinned recommended), intervals out; synchronous.
+
+        words/lens/out may be numpy arrays or pinned CPU torch tensors (anything with .ctypes or .data_ptr())."""
+        def hptr(a):
+            if a is None:
+                return None
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        Q, stride = words.shape
+        if out is None:
+            out = np.empty((Q, 2), dtype=np.uint32)
+        _check(lib().sa_match_batch_host(self._h, hptr(words), hptr(lens), int(fixed_len or 0), stride, Q, hptr(out),
+                                         int(chunk)), "sa_match_batch_host")
+        return out
+
+    def locate(self, lohi, stream=None) -> Tuple["object", "object"]:
+        """Positions SA[lo..hi) of every query (SA order).  Returns (offsets int64 [Q+1], positions int32 [total])."""
+        import torch
+        Q = lohi.shape[0]
+        dev = lohi.device
+        offsets = torch.empty(Q + 1, dtype=torch.int64, device=dev)
+        ws = _sz()
+        _check(lib().sa_locate_workspace_size(Q, ctypes.byref(ws)), "sa_locate_workspace_size")
+        wsb = torch.empty(max(1, ws.value), dtype=torch.uint8, device=dev)
+        sp = _stream_ptr(stream)
+        _check(lib().sa_locate_offsets(self._h, _dptr(lohi), Q, _dptr(offsets), _dptr(wsb), ws.value, sp),
+               "sa_locate_offsets")
+        total = int(offsets[Q].item())
+        positions = torch.empty(total, dtype=torch.int32, device=dev)
+        _check(lib().sa_locate(self._h, _dptr(lohi), _dptr(offsets), Q, _dptr(positions), sp), "sa_locate")
+        return offsets, positions
+
+
+def random_gather(device: int = 0, buffer_bytes: int = 16 << 30, access_bytes: int = 32, n_threads: int = 148 * 2048 * 4,
+                  loads: int = 64, dependent: bool = False) -> dict:
+    """Random-access gather microbenchmark (the roofline denominator for a random-gather kernel)."""
+    ms = ctypes.c_float()
+    _check(lib().sa_tool_random_gather(device, buffer_bytes, access_bytes, n_threads, loads, int(dependent),
+                                       ctypes.byref(ms)), "sa_tool_random_gather")
+    accesses = n_threads * loads
+    return {"ms": ms.value, "accesses": accesses, "access_bytes": access_bytes,
+            "GBps": accesses * access_bytes / (ms.value * 1e-3) / 1e9,
+            "Gaccess_per_s": accesses / (ms.value * 1e-3) / 1e9}

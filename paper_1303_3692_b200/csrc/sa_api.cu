@@ -1,0 +1,213 @@
+// sa_api.cu -- C ABI plumbing of libsa: errors, index lifetime, exports, measurement tool.
+#include <cstdarg>
+#include <cstring>
+#include <new>
+
+#include "sa_internal.cuh"
+
+static thread_local char g_err[512] = "";
+
+void sa_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+void sa_clear_error() { g_err[0] = 0; }
+
+extern "C" const char *sa_last_error(void) { return g_err; }
+extern "C" int32_t sa_version(void) { return 100; /* 0.1.0 */ }
+
+static void free_index(sa_index *idx) {
+    if (!idx) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(idx->device);
+    cudaDeviceSynchronize();
+    cudaFree(idx->text);
+    cudaFree(idx->sa);
+    cudaFree(idx->table);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(idx->pipe_words[b]);
+        cudaFree(idx->pipe_lens[b]);
+        cudaFree(idx->pipe_out[b]);
+        if (idx->pipe_stream[b]) cudaStreamDestroy(idx->pipe_stream[b]);
+    }
+    (void)cudaGetLastError();
+    cudaSetDevice(prev);
+    delete idx;
+}
+
+extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa_index_opts *opts, sa_index **out) {
+    sa_clear_error();
+    if (!out) { sa_set_error("out is NULL"); return SA_EINVAL; }
+    *out = nullptr;
+    if (n == 0) { sa_set_error("empty reference (n = 0)"); return SA_EEMPTY; }
+    if (!ref_ascii) { sa_set_error("ref_ascii is NULL"); return SA_EINVAL; }
+    if (n > 0xFFFFFFFFull) {
+        sa_set_error("reference of %llu bases exceeds 2^32-1 (uint32 suffix array)", (unsigned long long)n);
+        return SA_ETOOLONG;
+    }
+    sa_index_opts o{-1, 0, 0, 0};
+    if (opts) o = *opts;
+    if (o.flags != 0 || o.reserved != 0) { sa_set_error("opts.flags/reserved must be 0"); return SA_EINVAL; }
+    if (o.kmer_k > 16) { sa_set_error("kmer_k %u out of range 1..16", o.kmer_k); return SA_EINVAL; }
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        (void)cudaGetLastError();
+        sa_set_error("no CUDA device available (%s)", e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+        return SA_ECUDA;
+    }
+    int dev = o.device;
+    if (dev < 0) SA_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= ndev) { sa_set_error("device %d out of range (%d devices)", dev, ndev); return SA_EINVAL; }
+    int prev = 0;
+    SA_CUDA_TRY(cudaGetDevice(&prev));
+    SA_CUDA_TRY(cudaSetDevice(dev));
+
+    sa_index *idx = new (std::nothrow) sa_index();
+    if (!idx) { sa_set_error("host allocation failed"); cudaSetDevice(prev); return SA_ENOMEM; }
+    idx->device = dev;
+    idx->n = n;
+    uint32_t k = o.kmer_k;
+    if (k == 0) {  // auto: floor(log4 n), at most 12 (a 64 MiB table)
+        k = 1;
+        while (k < 12 && (1ull << (2 * (k + 1))) <= n) ++k;
+    }
+    idx->k = k;
+    cudaStream_t st = nullptr;
+    sa_status s = SA_OK;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+        (void)cudaGetLastError();
+        sa_set_error("stream creation failed");
+        s = SA_ECUDA;
+    }
+    if (s == SA_OK) s = sa_build_index(idx, ref_ascii, st);
+    if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    if (s != SA_OK) {
+        free_index(idx);
+        cudaSetDevice(prev);
+        return s;
+    }
+    cudaSetDevice(prev);
+    *out = idx;
+    return SA_OK;
+}
+
+extern "C" void sa_index_destroy(sa_index *idx) { free_index(idx); }
+
+extern "C" sa_status sa_index_info(const sa_index *idx, uint64_t *n, uint32_t *kmer_k, uint64_t *device_bytes,
+                                   int32_t *device) {
+    sa_clear_error();
+    if (!idx) { sa_set_error("index is NULL"); return SA_EINVAL; }
+    if (n) *n = idx->n;
+    if (kmer_k) *kmer_k = idx->k;
+    if (device_bytes) *device_bytes = idx->device_bytes;
+    if (device) *device = idx->device;
+    return SA_OK;
+}
+
+static sa_status export_copy(const sa_index *idx, void *dst, const void *src, size_t bytes) {
+    if (!idx || !dst) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    SA_CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return SA_OK;
+}
+
+extern "C" sa_status sa_index_export_sa(const sa_index *idx, uint32_t *host_out) {
+    sa_clear_error();
+    return export_copy(idx, host_out, idx ? idx->sa : nullptr, idx ? idx->n * sizeof(uint32_t) : 0);
+}
+
+extern "C" sa_status sa_index_export_table(const sa_index *idx, uint32_t *host_out) {
+    sa_clear_error();
+    return export_copy(idx, host_out, idx ? idx->table : nullptr,
+                       idx ? ((1ull << (2 * idx->k)) + 1) * sizeof(uint32_t) : 0);
+}
+
+extern "C" sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out) {
+    sa_clear_error();
+    return export_copy(idx, host_out, idx ? idx->text : nullptr, idx ? ((idx->n + 31) / 32) * sizeof(uint64_t) : 0);
+}
+
+// ---- measurement tool: random-access gather rate ---------------------------------------------
+__device__ __forceinline__ uint64_t hash64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <int BYTES>
+__global__ void k_gather(const uint8_t *__restrict__ buf, uint64_t slots, uint32_t loads, int dependent,
+                         uint64_t *__restrict__ sink) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t acc = 0;
+    uint64_t h = hash64(tid + 0x1234567ull);
+#pragma unroll 8
+    for (uint32_t i = 0; i < loads; ++i) {
+        const uint64_t slot = (dependent ? (h ^ acc) : hash64(h + i)) % slots;
+        const uint8_t *p = buf + slot * BYTES;
+        if constexpr (BYTES == 32) {
+            const ulonglong4 v = *reinterpret_cast<const ulonglong4 *>(p);  // 256-bit load (sm_100)
+            acc += v.x ^ v.y ^ v.z ^ v.w;
+        } else if constexpr (BYTES == 16) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+            acc += (uint64_t)v.x ^ v.y ^ v.z ^ v.w;
+        } else if constexpr (BYTES == 8) {
+            acc += __ldg(reinterpret_cast<const unsigned long long *>(p));
+        } else {
+            acc += __ldg(reinterpret_cast<const unsigned int *>(p));
+        }
+        if (dependent) h = hash64(h + acc);
+    }
+    if (acc == 0x5eed) sink[0] = acc;  // keeps the loads alive
+}
+
+extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes,
+                                           uint64_t n_threads, uint32_t loads, int32_t dependent, float *ms) {
+    sa_clear_error();
+    if (!ms || buffer_bytes < 4096 || n_threads == 0 || loads == 0 ||
+        !(access_bytes == 4 || access_bytes == 8 || access_bytes == 16 || access_bytes == 32)) {
+        sa_set_error("bad argument");
+        return SA_EINVAL;
+    }
+    SA_CUDA_TRY(cudaSetDevice(device));
+    uint8_t *buf = nullptr;
+    uint64_t *sink = nullptr;
+    SA_CUDA_TRY(cudaMalloc(&buf, buffer_bytes));
+    if (cudaMalloc(&sink, 8) != cudaSuccess) { cudaFree(buf); SA_CUDA_TRY(cudaGetLastError()); }
+    cudaMemset(buf, 0x5A, buffer_bytes);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const uint64_t slots = buffer_bytes / access_bytes;
+    const unsigned threads = 256;
+    const unsigned blocks = (unsigned)((n_threads + threads - 1) / threads);
+    auto launch = [&]() {
+        switch (access_bytes) {
+        case 32: k_gather<32><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
+        case 16: k_gather<16><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
+        case 8: k_gather<8><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
+        default: k_gather<4><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
+        }
+    };
+    launch();  // warm-up
+    cudaEventRecord(a);
+    launch();
+    cudaEventRecord(b);
+    cudaError_t e = cudaEventSynchronize(b);
+    float t = 0;
+    cudaEventElapsedTime(&t, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    cudaFree(sink);
+    SA_CUDA_TRY(e);
+    SA_CUDA_TRY(cudaGetLastError());
+    *ms = t;
+    return SA_OK;
+}

@@ -1,0 +1,336 @@
+// sa_build.cu -- index build (off the timed path): validate + pack the reference, build the suffix
+// array on the GPU, build the k-mer bracket table.
+//
+// The paper builds its suffix array on the CPU with DC3 (Sec. III).  Here the
+// same object -- SA, all suffix starts in lexicographic order with a proper prefix first
+// (Table I; reading A2) -- is built on the B200 by prefix doubling
+// (DESIGN.md "Index build"):
+//   round 0   key = the first 21 bases of each suffix at 3 bits/base (1..4 = a..t, 0 = past the
+//             end, so a suffix that ends inside the window carries its own terminator) -> one CUB
+//             radix sort of (key, position) over all n suffixes;
+//   round r   h = 21 * 2^(r-1): only suffixes still tied with a neighbour are re-sorted by
+//             (rank[s], rank[s+h]), rank = 1 + start of the suffix's group, rank[n] = 0.
+// Tied suffixes always have >= h bases (a terminator inside the window would have split them),
+// so s + h <= n and rank[] needs only one extra slot.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <cstring>
+#include <vector>
+
+#include "sa_internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(uint64_t n, int threads = kThreads) {
+    uint64_t b = (n + threads - 1) / threads;
+    const uint64_t cap = 148ull * 64;  // grid-stride beyond this
+    if (b > cap) b = cap;
+    if (b == 0) b = 1;
+    return (unsigned)b;
+}
+
+#define GRID_STRIDE(i, n) \
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (uint64_t)gridDim.x * blockDim.x)
+
+// ---- pack -------------------------------------------------------------------------------------
+// One thread per output word: 32 ASCII bytes -> 2-bit codes, MSB-first.  A=0 C=1 G=2 T=3 via
+// ((c>>1)&3) ^ ((c>>2)&1) (upper or lower case); anything else records its position.
+__global__ void k_pack(const uint8_t *__restrict__ ascii, uint64_t len, uint64_t base_word, uint64_t *__restrict__ text,
+                       unsigned long long *__restrict__ bad) {
+    const uint64_t words = (len + 31) / 32;
+    GRID_STRIDE(t, words) {
+        const uint64_t b0 = t * 32;
+        const unsigned cnt = (len - b0 < 32) ? (unsigned)(len - b0) : 32u;
+        uint64_t w = 0;
+        unsigned long long first_bad = ~0ull;
+        for (unsigned j = 0; j < cnt; ++j) {
+            const unsigned c = ascii[b0 + j];
+            const unsigned lc = c | 0x20u;
+            if (!(lc == 'a' || lc == 'c' || lc == 'g' || lc == 't')) {
+                if (first_bad == ~0ull) first_bad = (base_word * 32 + b0 + j);
+            }
+            const uint64_t code = ((c >> 1) & 3u) ^ ((c >> 2) & 1u);
+            w |= code << (62 - 2 * j);
+        }
+        text[base_word + t] = w;
+        if (first_bad != ~0ull) atomicMin(bad, first_bad);
+    }
+}
+
+// ---- suffix array: round 0 -------------------------------------------------------------------
+__global__ void k_init_keys(const uint64_t *__restrict__ text, uint64_t n, uint64_t *__restrict__ keys,
+                            uint32_t *__restrict__ vals) {
+    GRID_STRIDE(i, n) {
+        const uint64_t w = text_window(text, i);
+        uint64_t key = 0;
+#pragma unroll
+        for (int j = 0; j < 21; ++j) {
+            const uint64_t c = (i + j < n) ? ((w >> (62 - 2 * j)) & 3u) + 1u : 0u;
+            key = (key << 3) | c;
+        }
+        keys[i] = key;
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// head candidates: t where a new group starts (key differs from its left neighbour), else 0
+__global__ void k_head_cand(const uint64_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ cand) {
+    GRID_STRIDE(t, m) { cand[t] = (t == 0 || keys[t] != keys[t - 1]) ? (uint32_t)t : 0u; }
+}
+
+// active = member of a group of size > 1
+__global__ void k_active(const uint64_t *__restrict__ keys, uint64_t m, uint8_t *__restrict__ flags) {
+    GRID_STRIDE(t, m) {
+        const bool head = (t == 0 || keys[t] != keys[t - 1]);
+        const bool next_head = (t + 1 == m) || keys[t + 1] != keys[t];
+        flags[t] = (head && next_head) ? 0 : 1;
+    }
+}
+
+// round 0: rank[SA[r]] = head(r) + 1, rank[n] = 0
+__global__ void k_rank0(const uint32_t *__restrict__ sa, const uint32_t *__restrict__ head, uint64_t n,
+                        uint32_t *__restrict__ rank) {
+    GRID_STRIDE(r, n) { rank[sa[r]] = head[r] + 1u; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) rank[n] = 0;
+}
+
+// ---- suffix array: doubling rounds -----------------------------------------------------------
+__global__ void k_round_keys(const uint32_t *__restrict__ A, uint64_t nA, const uint32_t *__restrict__ sa,
+                             const uint32_t *__restrict__ rank, uint64_t h, uint64_t *__restrict__ keys,
+                             uint32_t *__restrict__ vals) {
+    GRID_STRIDE(t, nA) {
+        const uint32_t s = sa[A[t]];
+        keys[t] = ((uint64_t)rank[s] << 32) | rank[(uint64_t)s + h];
+        vals[t] = s;
+    }
+}
+
+__global__ void k_round_scatter(const uint32_t *__restrict__ A, uint64_t nA, const uint32_t *__restrict__ vals,
+                                const uint32_t *__restrict__ head, uint32_t *__restrict__ sa,
+                                uint32_t *__restrict__ rank) {
+    GRID_STRIDE(t, nA) {
+        const uint32_t s = vals[t];
+        sa[A[t]] = s;
+        rank[s] = A[head[t]] + 1u;
+    }
+}
+
+struct MaxU32 {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+// ---- k-mer bracket table ---------------------------------------------------------------------
+// e(r) = (number of k-mers x with x <= suffix SA[r]) - 1: the k-mer code of a suffix with >= k bases,
+// U-1 for a shorter suffix u whose a-padded k-mer is U (u > x  <=>  x < U).  e is non-decreasing
+// along the SA, and T[x] = #{r : e(r) < x} = r for e(r-1) < x <= e(r).
+__device__ __forceinline__ int64_t kmer_e(const uint64_t *__restrict__ text, uint64_t n, const uint32_t *__restrict__ sa,
+                                          uint64_t r, unsigned k) {
+    const uint64_t s = sa[r];
+    const uint64_t len = n - s;
+    uint64_t w = text_window(text, s);
+    if (len < k) w &= prefix_mask((unsigned)len);
+    const int64_t code = (int64_t)(w >> (64 - 2 * k));
+    return len >= k ? code : code - 1;
+}
+
+__global__ void k_table(const uint64_t *__restrict__ text, uint64_t n, const uint32_t *__restrict__ sa, unsigned k,
+                        uint32_t *__restrict__ T) {
+    const int64_t K = 1ll << (2 * k);
+    GRID_STRIDE(r, n + 1) {
+        const int64_t lo = (r == 0) ? 0 : kmer_e(text, n, sa, r - 1, k) + 1;
+        const int64_t hi = (r == n) ? K : kmer_e(text, n, sa, r, k);
+        for (int64_t x = lo; x <= hi; ++x) T[x] = (uint32_t)r;
+    }
+}
+
+template <typename F>
+sa_status cub_call(F f, cudaStream_t st, const char *what) {
+    size_t bytes = 0;
+    cudaError_t e = f(nullptr, bytes);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        sa_set_error("%s (size query): %s", what, cudaGetErrorString(e));
+        return SA_ECUDA;
+    }
+    DevBuf<uint8_t> tmp;
+    SA_TRY(tmp.alloc(bytes, st, what));
+    e = f(tmp.p, bytes);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        sa_set_error("%s: %s", what, cudaGetErrorString(e));
+        return SA_ECUDA;
+    }
+    return SA_OK;
+}
+
+// head[t] = last group start <= t, for sorted keys[0..m)
+sa_status group_heads(const uint64_t *keys, uint64_t m, uint32_t *head, cudaStream_t st) {
+    k_head_cand<<<grid_for(m), kThreads, 0, st>>>(keys, m, head);
+    SA_CUDA_TRY(cudaGetLastError());
+    return cub_call(
+        [&](void *tmp, size_t &bytes) {
+            return cub::DeviceScan::InclusiveScan(tmp, bytes, head, head, MaxU32(), (int64_t)m, st);
+        },
+        st, "group head scan");
+}
+
+// out[j] = in[t] for flagged t (order kept); returns the count.  out is sized m (transient).
+template <typename InIt>
+sa_status compact(InIt in, const uint8_t *flags, uint64_t m, DevBuf<uint32_t> &out, uint64_t &count,
+                  cudaStream_t st) {
+    DevBuf<int64_t> d_num;
+    SA_TRY(d_num.alloc(1, st, "compaction count"));
+    SA_TRY(out.alloc(m, st, "active list"));
+    SA_TRY(cub_call(
+        [&](void *tmp, size_t &bytes) {
+            return cub::DeviceSelect::Flagged(tmp, bytes, in, flags, out.p, d_num.p, (int64_t)m, st);
+        },
+        st, "compaction"));
+    int64_t h_num = 0;
+    SA_CUDA_TRY(cudaMemcpyAsync(&h_num, d_num.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    count = (uint64_t)h_num;
+    return SA_OK;
+}
+
+sa_status sort_pairs(uint64_t *&keys, uint64_t *keys_alt, uint32_t *&vals, uint32_t *vals_alt, uint64_t m,
+                     int end_bit, cudaStream_t st) {
+    cub::DoubleBuffer<uint64_t> dk(keys, keys_alt);
+    cub::DoubleBuffer<uint32_t> dv(vals, vals_alt);
+    SA_TRY(cub_call(
+        [&](void *tmp, size_t &bytes) {
+            return cub::DeviceRadixSort::SortPairs(tmp, bytes, dk, dv, (int64_t)m, 0, end_bit, st);
+        },
+        st, "radix sort"));
+    keys = dk.Current();
+    vals = dv.Current();
+    return SA_OK;
+}
+
+sa_status build_sa(sa_index *idx, cudaStream_t st) {
+    const uint64_t n = idx->n;
+    uint32_t *sa = idx->sa;
+    DevBuf<uint32_t> rank, A;
+    uint64_t nA = 0;
+    {   // round 0
+        DevBuf<uint64_t> ka, kb;
+        DevBuf<uint32_t> vb;
+        SA_TRY(ka.alloc(n, st, "round-0 keys"));
+        SA_TRY(kb.alloc(n, st, "round-0 keys (alt)"));
+        SA_TRY(vb.alloc(n, st, "round-0 values (alt)"));
+        k_init_keys<<<grid_for(n), kThreads, 0, st>>>(idx->text, n, ka.p, sa);
+        SA_CUDA_TRY(cudaGetLastError());
+        uint64_t *keys = ka.p;
+        uint32_t *vals = sa;
+        SA_TRY(sort_pairs(keys, kb.p, vals, vb.p, n, 63, st));
+        if (vals != sa) SA_CUDA_TRY(cudaMemcpyAsync(sa, vals, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        uint32_t *head = vb.p;  // reuse: vals now live in sa
+        SA_TRY(group_heads(keys, n, head, st));
+        SA_TRY(rank.alloc(n + 1, st, "rank"));
+        k_rank0<<<grid_for(n), kThreads, 0, st>>>(sa, head, n, rank.p);
+        SA_CUDA_TRY(cudaGetLastError());
+        DevBuf<uint8_t> flags;
+        SA_TRY(flags.alloc(n, st, "active flags"));
+        k_active<<<grid_for(n), kThreads, 0, st>>>(keys, n, flags.p);
+        SA_CUDA_TRY(cudaGetLastError());
+        vb.reset();
+        ka.reset();
+        kb.reset();
+        SA_TRY(compact(thrust::counting_iterator<uint32_t>(0), flags.p, n, A, nA, st));
+    }
+    uint64_t h = 21;
+    uint32_t rounds = 0;
+    while (nA > 0) {
+        if (h >= n || rounds > 40) {
+            sa_set_error("suffix array build did not converge (h=%llu, %llu tied suffixes)",
+                         (unsigned long long)h, (unsigned long long)nA);
+            return SA_ECUDA;
+        }
+        DevBuf<uint64_t> ka, kb;
+        DevBuf<uint32_t> va, vb, head;
+        SA_TRY(ka.alloc(nA, st, "round keys"));
+        SA_TRY(kb.alloc(nA, st, "round keys (alt)"));
+        SA_TRY(va.alloc(nA, st, "round values"));
+        SA_TRY(vb.alloc(nA, st, "round values (alt)"));
+        k_round_keys<<<grid_for(nA), kThreads, 0, st>>>(A.p, nA, sa, rank.p, h, ka.p, va.p);
+        SA_CUDA_TRY(cudaGetLastError());
+        uint64_t *keys = ka.p;
+        uint32_t *vals = va.p;
+        SA_TRY(sort_pairs(keys, kb.p, vals, vb.p, nA, 64, st));
+        SA_TRY(head.alloc(nA, st, "round heads"));
+        SA_TRY(group_heads(keys, nA, head.p, st));
+        k_round_scatter<<<grid_for(nA), kThreads, 0, st>>>(A.p, nA, vals, head.p, sa, rank.p);
+        SA_CUDA_TRY(cudaGetLastError());
+        DevBuf<uint8_t> flags;
+        SA_TRY(flags.alloc(nA, st, "active flags"));
+        k_active<<<grid_for(nA), kThreads, 0, st>>>(keys, nA, flags.p);
+        SA_CUDA_TRY(cudaGetLastError());
+        head.reset();
+        ka.reset();
+        kb.reset();
+        va.reset();
+        vb.reset();
+        DevBuf<uint32_t> A2;
+        uint64_t nA2 = 0;
+        SA_TRY(compact(A.p, flags.p, nA, A2, nA2, st));
+        A.reset();
+        A.p = A2.release();
+        A.count = nA2;
+        A.st = st;
+        nA = nA2;
+        h *= 2;
+        ++rounds;
+    }
+    idx->build_rounds = rounds;
+    return SA_OK;
+}
+
+}  // namespace
+
+sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) {
+    const uint64_t n = idx->n;
+    // ---- 1. upload + validate + pack (chunks of 256 MiB) ----
+    idx->n_words = (n + 31) / 32 + 2;
+    SA_CUDA_TRY(cudaMalloc(&idx->text, idx->n_words * sizeof(uint64_t)));
+    SA_CUDA_TRY(cudaMemsetAsync(idx->text, 0, idx->n_words * sizeof(uint64_t), st));
+    {
+        const uint64_t CH = 256ull << 20;
+        DevBuf<uint8_t> dbuf;
+        DevBuf<unsigned long long> bad;
+        SA_TRY(dbuf.alloc(n < CH ? n : CH, st, "upload staging"));
+        SA_TRY(bad.alloc(1, st, "validation flag"));
+        SA_CUDA_TRY(cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), st));
+        for (uint64_t off = 0; off < n; off += CH) {
+            const uint64_t len = (n - off < CH) ? n - off : CH;
+            SA_CUDA_TRY(cudaMemcpyAsync(dbuf.p, ref_ascii + off, len, cudaMemcpyHostToDevice, st));
+            k_pack<<<grid_for((len + 31) / 32), kThreads, 0, st>>>(dbuf.p, len, off / 32, idx->text, bad.p);
+            SA_CUDA_TRY(cudaGetLastError());
+        }
+        unsigned long long h_bad = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad.p, sizeof(h_bad), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h_bad != ~0ull) {
+            const unsigned char c = (unsigned char)ref_ascii[h_bad];
+            sa_set_error("reference symbol 0x%02x ('%c') at position %llu is not A/C/G/T", c,
+                         (c >= 32 && c < 127) ? c : '?', h_bad);
+            return SA_ESYMBOL;
+        }
+    }
+    // ---- 2. suffix array ----
+    SA_CUDA_TRY(cudaMalloc(&idx->sa, n * sizeof(uint32_t)));
+    SA_TRY(build_sa(idx, st));
+    // ---- 3. k-mer bracket table ----
+    const uint64_t K = 1ull << (2 * idx->k);
+    SA_CUDA_TRY(cudaMalloc(&idx->table, (K + 1) * sizeof(uint32_t)));
+    k_table<<<grid_for(n + 1), kThreads, 0, st>>>(idx->text, n, idx->sa, idx->k, idx->table);
+    SA_CUDA_TRY(cudaGetLastError());
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    idx->device_bytes = idx->n_words * 8 + n * 4 + (K + 1) * 4;
+    // hand the build's transient memory back to the driver
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    return SA_OK;
+}

@@ -1,0 +1,111 @@
+// sa_internal.cuh -- private types and device helpers of libsa (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "sa.h"
+
+// ---------------------------------------------------------------------------------------------
+// errors
+void sa_set_error(const char *fmt, ...);
+void sa_clear_error();
+
+#define SA_CUDA_TRY(call)                                                                              \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) {                                                                       \
+            (void)cudaGetLastError();                                                                  \
+            sa_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));          \
+            return e_ == cudaErrorMemoryAllocation ? SA_ENOMEM : SA_ECUDA;                             \
+        }                                                                                              \
+    } while (0)
+
+#define SA_TRY(call)                                                                                   \
+    do {                                                                                               \
+        sa_status s_ = (call);                                                                         \
+        if (s_ != SA_OK) return s_;                                                                    \
+    } while (0)
+
+// RAII device buffer (stream-ordered allocator); freed on scope exit.
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t count = 0;
+    cudaStream_t st = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { reset(); }
+    sa_status alloc(size_t n, cudaStream_t s, const char *what) {
+        reset();
+        st = s;
+        if (n == 0) n = 1;
+        cudaError_t e = cudaMallocAsync((void **)&p, n * sizeof(T), s);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            p = nullptr;
+            sa_set_error("device allocation of %zu bytes for %s failed: %s", n * sizeof(T), what,
+                         cudaGetErrorString(e));
+            return e == cudaErrorMemoryAllocation ? SA_ENOMEM : SA_ECUDA;
+        }
+        count = n;
+        return SA_OK;
+    }
+    void reset() {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+        count = 0;
+    }
+    T *release() {
+        T *r = p;
+        p = nullptr;
+        count = 0;
+        return r;
+    }
+};
+
+// ---------------------------------------------------------------------------------------------
+// the index (immutable after create)
+struct sa_index {
+    int device = 0;
+    uint64_t n = 0;          // reference length
+    uint32_t k = 0;          // k-mer bracket table
+    uint64_t n_words = 0;    // packed text words incl. 2 zero guard words
+    uint64_t *text = nullptr;    // dev: 2-bit MSB-first, zero-padded past n
+    uint32_t *sa = nullptr;      // dev: n entries
+    uint32_t *table = nullptr;   // dev: 4^k + 1 entries
+    uint64_t device_bytes = 0;
+    uint32_t build_rounds = 0;   // prefix-doubling rounds after the initial sort
+    // host-buffer pipeline (sa_match_batch_host); grown on demand, guarded by mu
+    std::mutex mu;
+    cudaStream_t pipe_stream[2] = {nullptr, nullptr};
+    uint64_t *pipe_words[2] = {nullptr, nullptr};
+    uint32_t *pipe_lens[2] = {nullptr, nullptr};
+    uint32_t *pipe_out[2] = {nullptr, nullptr};
+    uint64_t pipe_chunk = 0;
+    uint32_t pipe_stride = 0;
+};
+
+// ---------------------------------------------------------------------------------------------
+// device helpers
+
+// 32 bases of the packed text starting at base b (b < n + 32); bases past n read as 0 ('a').
+__device__ __forceinline__ uint64_t text_window(const uint64_t *__restrict__ text, uint64_t b) {
+    const uint64_t w = b >> 5;
+    const unsigned sh = (unsigned)(b & 31u) << 1;
+    const uint64_t x0 = __ldg(reinterpret_cast<const unsigned long long *>(text) + w);
+    const uint64_t x1 = __ldg(reinterpret_cast<const unsigned long long *>(text) + w + 1);
+    return sh ? (x0 << sh) | (x1 >> (64u - sh)) : x0;
+}
+
+// mask selecting the first L (0..32) bases of a packed word
+__device__ __forceinline__ uint64_t prefix_mask(unsigned L) {
+    return L >= 32 ? ~0ull : (L == 0 ? 0ull : ~(~0ull >> (2u * L)));
+}
+
+// build / match entry points implemented in sa_build.cu / sa_match.cu
+sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st);

@@ -1,0 +1,363 @@
+// sa_match.cu -- the hot path: per-query SA interval [lo, hi) by binary search (Sec. IV,
+// Alg. 1 `cudaGeneBinSearch`, L173-230), plus locate and the host-buffer pipeline.
+//
+// B200 design, not a translation of Alg. 1:
+//  * one thread per query (Alg. 1 line 2's mapping) with the query held in registers
+//    (2 bits/base, MSB-first words) instead of the per-block shared tiles of lines 5, 14-15 (which
+//    race as written, reading A9);
+//  * the first k bases index the k-mer bracket table T: the search starts in
+//    (T[x]-1, T[x+1]) instead of Alg. 1's (left, right) = (-1, n) (reading A4);
+//  * Alg. 1's tiled do-while compare (lines 10-17) becomes a 32-bases-per-step compare of two
+//    packed words (xor + clz; unsigned order of MSB-first words is lexicographic order);
+//  * the LB and RB loops (lines 6-23 and 25-42, directions corrected per reading A6) run jointly:
+//    one descent until the first pivot equal to P, then the RB search continues from that split;
+//  * Manber-Myers skipping: compares start at min(lcp(P, t_L), lcp(P, t_R)).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include <algorithm>
+
+#include "sa_internal.cuh"
+
+namespace {
+
+struct MatchArgs {
+    const uint64_t *__restrict__ text;
+    const uint32_t *__restrict__ sa;
+    const uint32_t *__restrict__ table;
+    uint64_t n;
+    uint32_t k;
+    const uint64_t *__restrict__ words;
+    const uint32_t *__restrict__ lens;
+    uint32_t fixed_len;
+    uint32_t stride;
+    uint64_t Q;
+    uint32_t *__restrict__ out;
+};
+
+// Query words: QW > 0 -> registers (fully unrolled so indices are static); QW == 0 -> global.
+template <int QW>
+struct QueryWords {
+    uint64_t w[QW];
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw) {
+#pragma unroll
+        for (int j = 0; j < QW; ++j) w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+    }
+    __device__ __forceinline__ uint64_t first() const { return w[0]; }
+};
+template <>
+struct QueryWords<0> {
+    const uint64_t *p;
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t) { p = q; }
+    __device__ __forceinline__ uint64_t first() const { return __ldg(reinterpret_cast<const unsigned long long *>(p)); }
+};
+
+// One 32-base step of the compare: word j of P against the text at s + 32j.
+// Returns 1 when decided (sign/lcp set), 0 to continue.
+__device__ __forceinline__ int cmp_word(const uint64_t *__restrict__ text, uint64_t s, uint64_t slen, uint32_t m,
+                                        uint32_t j, uint64_t pw, int &sign, uint32_t &lcp) {
+    const uint32_t base = j << 5;
+    const uint32_t plen = min(32u, m - base);
+    const uint64_t rem = slen > base ? slen - base : 0;
+    const uint32_t L = rem < plen ? (uint32_t)rem : plen;
+    if (L) {
+        const uint64_t tw = text_window(text, s + base);
+        const uint64_t mask = prefix_mask(L);
+        const uint64_t a = pw & mask, b = tw & mask;
+        if (a != b) {
+            lcp = base + ((uint32_t)__clzll((long long)(a ^ b)) >> 1);
+            sign = a > b ? 1 : -1;
+            return 1;
+        }
+    }
+    if (L < plen) {  // the suffix ended first: it is a proper prefix of P (reading A7)
+        lcp = base + L;
+        sign = 1;
+        return 1;
+    }
+    return 0;
+}
+
+// sign(P - t_s), t_s = S[s .. min(s+m, n)), comparing from word skip/32 on; lcp = lcp(P, t_s).
+template <int QW>
+__device__ __forceinline__ void compare(const uint64_t *__restrict__ text, uint64_t n, uint64_t s,
+                                        const QueryWords<QW> &P, uint32_t m, uint32_t skip, int &sign,
+                                        uint32_t &lcp) {
+    const uint64_t slen = n - s;
+    const uint32_t nw = (m + 31) >> 5;
+    const uint32_t j0 = skip >> 5;
+    if constexpr (QW > 0) {
+#pragma unroll
+        for (int j = 0; j < QW; ++j) {
+            if ((uint32_t)j >= j0 && (uint32_t)j < nw) {
+                if (cmp_word(text, s, slen, m, (uint32_t)j, P.w[j], sign, lcp)) return;
+            }
+        }
+    } else {
+        for (uint32_t j = j0; j < nw; ++j) {
+            const uint64_t pw = __ldg(reinterpret_cast<const unsigned long long *>(P.p) + j);
+            if (cmp_word(text, s, slen, m, j, pw, sign, lcp)) return;
+        }
+    }
+    sign = 0;
+    lcp = m;
+}
+
+// Binary search over (L, R) for the boundary where `P <= t` (lower = true, Alg. 1 LB loop) or
+// `P < t` (lower = false, RB loop) starts; returns R.
+template <int QW>
+__device__ __forceinline__ int64_t bound(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, int64_t L,
+                                         int64_t R, uint32_t lcpL, uint32_t lcpR, bool lower) {
+    while (R - L > 1) {
+        const int64_t p = (L + R) >> 1;
+        const uint64_t s = __ldg(a.sa + p);
+        int sign;
+        uint32_t lcp;
+        compare<QW>(a.text, a.n, s, P, m, min(lcpL, lcpR), sign, lcp);
+        const bool go_left = lower ? (sign <= 0) : (sign < 0);
+        if (go_left) { R = p; lcpR = lcp; } else { L = p; lcpL = lcp; }
+    }
+    return R;
+}
+
+template <int QW>
+__global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= a.Q) return;
+    // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
+    const uint32_t m = min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
+    const uint32_t nw = (m + 31) >> 5;
+    QueryWords<QW> P;
+    P.load(a.words + q * a.stride, nw);
+    int64_t lo, hi;
+    const uint32_t k = a.k;
+    if (m == 0) {  // the empty query is a prefix of every suffix (reading A12)
+        lo = 0;
+        hi = (int64_t)a.n;
+    } else if (m >= k) {
+        // all suffixes before T[x] are < P, all from T[x+1] on are > P
+        const uint64_t x = P.first() >> (64 - 2 * k);
+        int64_t L = (int64_t)__ldg(a.table + x) - 1;
+        int64_t R = (int64_t)__ldg(a.table + x + 1);
+        uint32_t lcpL = 0, lcpR = 0;
+        int64_t sL = -2, sR = 0;  // split: first pivot with P a prefix of its suffix
+        uint32_t slcpR = 0;
+        while (R - L > 1) {
+            const int64_t p = (L + R) >> 1;
+            const uint64_t s = __ldg(a.sa + p);
+            int sign;
+            uint32_t lcp;
+            compare<QW>(a.text, a.n, s, P, m, min(lcpL, lcpR), sign, lcp);
+            if (sign > 0) {
+                L = p;
+                lcpL = lcp;
+            } else {
+                if (sign == 0 && sL == -2) { sL = p; sR = R; slcpR = lcpR; }
+                R = p;
+                lcpR = lcp;
+            }
+        }
+        lo = R;
+        hi = (sL == -2) ? lo : bound<QW>(a, P, m, sL, sR, m, slcpR, false);
+    } else {
+        // m < k: lo lies in [T[xa]-k, T[xa]] and hi in [T[xb]-k, T[xb]], xa = x.a^(k-m),
+        // xb = (x+1).a^(k-m)
+        const uint64_t x = P.first() >> (64 - 2 * m);
+        const uint64_t xa = x << (2 * (k - m)), xb = (x + 1) << (2 * (k - m));
+        const int64_t Ta = (int64_t)__ldg(a.table + xa), Tb = (int64_t)__ldg(a.table + xb);
+        lo = bound<QW>(a, P, m, (Ta > (int64_t)k ? Ta - (int64_t)k : 0) - 1, Ta, 0, 0, true);
+        hi = bound<QW>(a, P, m, (Tb > (int64_t)k ? Tb - (int64_t)k : 0) - 1, Tb, 0, 0, false);
+    }
+    // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
+    reinterpret_cast<uint2 *>(a.out)[q] = make_uint2((uint32_t)lo, (uint32_t)hi);
+}
+
+template <int QW>
+cudaError_t launch_match(const MatchArgs &a, cudaStream_t st) {
+    const int threads = 256;
+    const uint64_t blocks = (a.Q + threads - 1) / threads;
+    k_match<QW><<<(unsigned)blocks, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---- locate -----------------------------------------------------------------------------------
+struct CountOp {
+    const uint32_t *lohi;
+    uint64_t Q;
+    __host__ __device__ __forceinline__ uint64_t operator()(uint64_t q) const {
+        return q < Q ? (uint64_t)(lohi[2 * q + 1] - lohi[2 * q]) : 0ull;
+    }
+};
+
+// One warp per query: lanes copy SA[lo .. hi) to positions[off ..] (contiguous, coalesced).
+__global__ void k_locate(const uint32_t *__restrict__ sa, const uint32_t *__restrict__ lohi,
+                         const uint64_t *__restrict__ offsets, uint64_t Q, uint32_t *__restrict__ pos) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t q = warp; q < Q; q += nwarps) {
+        const uint32_t lo = lohi[2 * q], hi = lohi[2 * q + 1];
+        const uint64_t off = offsets[q];
+        for (uint64_t j = lane; j < (uint64_t)(hi - lo); j += 32) pos[off + j] = __ldg(sa + lo + j);
+    }
+}
+
+sa_status check_match_args(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                           uint32_t stride, uint64_t Q, const uint32_t *out) {
+    if (!idx) { sa_set_error("index is NULL"); return SA_EINVAL; }
+    if (Q == 0) return SA_OK;
+    if (!q_words || !out) { sa_set_error("q_words/out_lohi NULL with Q=%llu", (unsigned long long)Q); return SA_EINVAL; }
+    if (stride == 0) { sa_set_error("stride_words must be >= 1"); return SA_EINVAL; }
+    if (!q_len && fixed_len > 32u * stride) {
+        sa_set_error("fixed_len %u exceeds 32*stride_words = %u", fixed_len, 32u * stride);
+        return SA_EINVAL;
+    }
+    if (!q_len && fixed_len > 65535u) { sa_set_error("query length %u > 65535", fixed_len); return SA_EINVAL; }
+    return SA_OK;
+}
+
+}  // namespace
+
+// ---- C ABI ------------------------------------------------------------------------------------
+extern "C" sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, size_t *bytes) {
+    sa_clear_error();
+    if (!idx || !bytes) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    (void)Q;
+    (void)stride_words;
+    *bytes = 0;
+    return SA_OK;
+}
+
+static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                              uint32_t stride, uint64_t Q, uint32_t *out, cudaStream_t st) {
+    MatchArgs a;
+    a.text = idx->text;
+    a.sa = idx->sa;
+    a.table = idx->table;
+    a.n = idx->n;
+    a.k = idx->k;
+    a.words = q_words;
+    a.lens = q_len;
+    a.fixed_len = fixed_len;
+    a.stride = stride;
+    a.Q = Q;
+    a.out = out;
+    cudaError_t e;
+    if (stride <= 1) e = launch_match<1>(a, st);
+    else if (stride <= 2) e = launch_match<2>(a, st);
+    else if (stride <= 4) e = launch_match<4>(a, st);
+    else e = launch_match<0>(a, st);
+    if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+    return SA_OK;
+}
+
+extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
+                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t *out_lohi,
+                                    void *workspace, size_t ws_bytes, uint32_t flags, void *stream) {
+    sa_clear_error();
+    (void)workspace;
+    (void)ws_bytes;
+    SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
+    if (flags != 0) { sa_set_error("flags must be 0"); return SA_EINVAL; }
+    if (Q == 0) return SA_OK;
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, (cudaStream_t)stream);
+}
+
+extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
+                                         uint32_t fixed_len, uint32_t stride, uint64_t Q, uint32_t *out_lohi,
+                                         uint64_t chunk_Q) {
+    sa_clear_error();
+    SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride, Q, out_lohi));
+    if (Q == 0) return SA_OK;
+    std::lock_guard<std::mutex> lock(idx->mu);
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    if (chunk_Q == 0) chunk_Q = 1ull << 22;
+    if (chunk_Q > Q) chunk_Q = Q;
+    if (idx->pipe_chunk < chunk_Q || idx->pipe_stride < stride) {
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(idx->pipe_words[b]);
+            cudaFree(idx->pipe_lens[b]);
+            cudaFree(idx->pipe_out[b]);
+            idx->pipe_words[b] = nullptr;
+            idx->pipe_lens[b] = nullptr;
+            idx->pipe_out[b] = nullptr;
+        }
+        idx->pipe_chunk = 0;
+        for (int b = 0; b < 2; ++b) {
+            if (!idx->pipe_stream[b]) SA_CUDA_TRY(cudaStreamCreateWithFlags(&idx->pipe_stream[b], cudaStreamNonBlocking));
+            SA_CUDA_TRY(cudaMalloc(&idx->pipe_words[b], chunk_Q * stride * sizeof(uint64_t)));
+            SA_CUDA_TRY(cudaMalloc(&idx->pipe_lens[b], chunk_Q * sizeof(uint32_t)));
+            SA_CUDA_TRY(cudaMalloc(&idx->pipe_out[b], chunk_Q * 2 * sizeof(uint32_t)));
+        }
+        idx->pipe_chunk = chunk_Q;
+        idx->pipe_stride = stride;
+    }
+    // chunk c uses buffer set c%2 on stream c%2: H2D -> match -> D2H; the two streams overlap.
+    uint64_t c = 0;
+    for (uint64_t q0 = 0; q0 < Q; q0 += chunk_Q, ++c) {
+        const int b = (int)(c & 1);
+        cudaStream_t st = idx->pipe_stream[b];
+        const uint64_t cq = std::min<uint64_t>(chunk_Q, Q - q0);
+        SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_words[b], q_words + q0 * stride, cq * stride * sizeof(uint64_t),
+                                    cudaMemcpyHostToDevice, st));
+        const uint32_t *dl = nullptr;
+        if (q_len) {
+            SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            dl = idx->pipe_lens[b];
+        }
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], st));
+        SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    SA_CUDA_TRY(cudaStreamSynchronize(idx->pipe_stream[0]));
+    SA_CUDA_TRY(cudaStreamSynchronize(idx->pipe_stream[1]));
+    return SA_OK;
+}
+
+extern "C" sa_status sa_locate_workspace_size(uint64_t Q, size_t *bytes) {
+    sa_clear_error();
+    if (!bytes) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    CountOp op{nullptr, Q};
+    thrust::transform_iterator<CountOp, thrust::counting_iterator<uint64_t>, uint64_t> it(
+        thrust::counting_iterator<uint64_t>(0), op);
+    size_t b = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, b, it, (uint64_t *)nullptr, (int64_t)(Q + 1));
+    if (e != cudaSuccess) { sa_set_error("scan size: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+    *bytes = b;
+    return SA_OK;
+}
+
+extern "C" sa_status sa_locate_offsets(const sa_index *idx, const uint32_t *out_lohi, uint64_t Q, uint64_t *offsets,
+                                       void *workspace, size_t ws_bytes, void *stream) {
+    sa_clear_error();
+    if (!idx || !offsets || (Q > 0 && !out_lohi)) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    CountOp op{out_lohi, Q};
+    thrust::transform_iterator<CountOp, thrust::counting_iterator<uint64_t>, uint64_t> it(
+        thrust::counting_iterator<uint64_t>(0), op);
+    size_t need = 0;
+    SA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, it, offsets, (int64_t)(Q + 1), (cudaStream_t)stream));
+    if (ws_bytes < need || (need > 0 && !workspace)) {
+        sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, need);
+        return SA_EINVAL;
+    }
+    SA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(workspace, need, it, offsets, (int64_t)(Q + 1), (cudaStream_t)stream));
+    return SA_OK;
+}
+
+extern "C" sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_t *offsets, uint64_t Q,
+                               uint32_t *positions, void *stream) {
+    sa_clear_error();
+    if (!idx) { sa_set_error("index is NULL"); return SA_EINVAL; }
+    if (Q == 0) return SA_OK;
+    // positions may be NULL only when offsets[Q] == 0 (nothing is written then)
+    if (!out_lohi || !offsets) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    uint64_t blocks = (Q * 32 + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    k_locate<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(idx->sa, out_lohi, offsets, Q, positions);
+    SA_CUDA_TRY(cudaGetLastError());
+    return SA_OK;
+}

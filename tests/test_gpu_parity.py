@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Index: the GPU suffix array must equal the oracle's comparison-sort SA (small / medium sizes) or
+pass the oracle's SA check (permutation + strictly increasing adjacent suffixes) at full size; the
+k-mer table must equal the oracle's histogram table.  Match: every (lo, hi) must equal the
+oracle's textbook search (bit-exact, integers); at full size, a seeded sample is compared with the
+oracle's streaming counting oracle (no SA) and every query passes the oracle's certificate.
+"""
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+import paper_1303_3692_b200 as sa  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _text(s):
+    return s.encode("ascii") if isinstance(s, str) else s
+
+
+def gpu_match(idx, words, lens=None, fixed_len=None):
+    w = torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).cuda()
+    l = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).cuda()
+    out = idx.match(w, l, fixed_len=fixed_len)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32)
+
+
+def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True):
+    """Build on the GPU; compare SA, table and every interval with the oracle."""
+    S = oracle.encode(text_ascii)
+    idx = sa.Index(text_ascii, k=k)
+    sa_ref = oracle.sa_naive(S)
+    if check_sa:
+        assert np.array_equal(idx.export_sa(), sa_ref)
+    if idx.k <= 8:
+        assert np.array_equal(idx.export_table(), oracle.kmer_table(S, idx.k))
+    if queries is not None:
+        words, lens = synth.pack_strings(queries)
+    got = gpu_match(idx, words, lens)
+    want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
+    bad = np.nonzero((got != want).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first q={bad[0]}: got {got[bad[0]]} want {want[bad[0]]}"
+    return idx, S, sa_ref, got
+
+
+def hazard_queries(text, k, rng, extra=200):
+    n = len(text)
+    qs = ["", text[: min(n, 40)], text[-1:] + "t"]
+    for j in range(1, k + 3):
+        if j <= n:
+            qs.append(text[n - j:])                 # the last j bases
+            qs.append(text[n - j:] + "A")           # running past the end
+            qs.append(text[n - j:] + "T")
+    for m in sorted({1, max(1, k - 1), k, k + 1, 31, 32, 33, 63, 64, 65, 100, 127, 128}):
+        qs.append("A" * m)
+        qs.append("T" * m)
+        if m <= n:
+            i = rng.randrange(n - m + 1)
+            qs.append(text[i:i + m])
+            s = text[i:i + m]
+            j = rng.randrange(m)
+            qs.append(s[:j] + "ACGT".replace(s[j], "")[rng.randrange(3)] + s[j + 1:])
+        qs.append("".join(rng.choice("ACGT") for _ in range(m)))
+    for _ in range(extra):
+        m = rng.randint(1, 128)
+        if m <= n and rng.random() < 0.7:
+            i = rng.randrange(n - m + 1)
+            qs.append(text[i:i + m])
+        else:
+            qs.append("".join(rng.choice("ACGT") for _ in range(m)))
+    qs += qs[:10]  # duplicates
+    return qs
+
+
+# ---- the paper's worked example --------------------------------------------------------------
+
+def test_paper_example_table1_and_sec4():
+    idx = sa.Index("acggtacgtac")
+    assert idx.export_sa().tolist() == [9, 0, 5, 10, 1, 6, 2, 7, 3, 8, 4]   # Table I
+    words, lens = synth.pack_strings(["a", "c", "ggtac", "tac", "tt", "gg", "acggtacgtac", ""])
+    got = gpu_match(idx, words, lens)
+    assert got.tolist() == [[0, 3], [3, 6], [6, 7], [9, 11], [11, 11], [6, 7], [1, 2], [0, 11]]
+    offs, pos = idx.locate(torch.from_numpy(got.view(np.int32)).cuda())
+    assert pos.cpu().numpy()[:3].tolist() == [9, 0, 5]  # "namely 9, 0, 5"
+
+
+# ---- small adversarial texts: SA, table and intervals bit-exact --------------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 63, 64, 65, 1000, 4097])
+@pytest.mark.parametrize("k", [0, 1, 3, 6])
+def test_random_texts_all_k(n, k):
+    rng = random.Random(n * 10 + k)
+    text = "".join(rng.choice("ACGT") for _ in range(n))
+    check_full(text, hazard_queries(text, k or 6, rng), k=k)
+
+
+@pytest.mark.parametrize("text", [
+    "A" * 5000,
+    "AC" * 3000,
+    "ACGT" * 1500 + "A",
+    "T" * 777 + "A" * 333,
+    "ACGTTGCA" * 900,
+])
+def test_periodic_and_homopolymer_texts(text):
+    rng = random.Random(len(text))
+    check_full(text, hazard_queries(text, 8, rng), k=8)
+
+
+def test_homopolymer_closed_form():
+    n = 3000
+    idx = sa.Index("A" * n, k=5)
+    assert idx.export_sa().tolist() == list(range(n - 1, -1, -1))
+    ks = [1, 2, 4, 5, 6, 100, 2999, 3000]
+    words, lens = synth.pack_strings(["A" * kk for kk in ks])
+    got = gpu_match(idx, words, lens)
+    assert got.tolist() == [[kk - 1, n] for kk in ks]
+
+
+def de_bruijn(k):
+    a = [0] * (4 * k)
+    seq = []
+
+    def db(t, p):
+        if t > k:
+            if k % p == 0:
+                seq.extend(a[1:p + 1])
+        else:
+            a[t] = a[t - p]
+            db(t + 1, p)
+            for j in range(a[t - p] + 1, 4):
+                a[t] = j
+                db(t + 1, t)
+
+    db(1, 1)
+    s = "".join("ACGT"[i] for i in seq)
+    return s + s[:k - 1]
+
+
+def test_de_bruijn_every_kmer_once():
+    kk = 6
+    text = de_bruijn(kk)
+    kmers = ["".join(p) for p in itertools.product("ACGT", repeat=kk)]
+    idx, S, sa_ref, got = check_full(text, kmers, k=4)
+    assert np.all(got[:, 1] - got[:, 0] == 1)
+
+
+def test_short_queries_below_k():
+    # m < k exercises the widened brackets
+    rng = random.Random(7)
+    for n in [20, 300, 5000]:
+        text = "".join(rng.choice("AC") for _ in range(n)) + "".join(rng.choice("ACGT") for _ in range(n))
+        qs = ["".join(p) for m in range(1, 5) for p in itertools.product("ACGT", repeat=m)]
+        qs += [text[-j:] for j in range(1, 12)]
+        check_full(text, qs, k=10)
+
+
+def test_symbol_error_reports_position():
+    with pytest.raises(sa.SAError) as e:
+        sa.Index("ACGTACGTNACGT")
+    assert e.value.code == sa.SA_ESYMBOL and "position 8" in e.value.detail
+
+
+def test_lowercase_reference():
+    text = "acggtacgtac"
+    assert sa.Index(text.upper()).export_sa().tolist() == sa.Index(text).export_sa().tolist()
+
+
+# ---- BASELINE.json configs ----------------------------------------------------------------------
+
+def test_c1_full_parity():
+    c = synth.CONFIGS["C1"]
+    ref = c.reference()
+    words, lens = c.reads(ref)
+    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens)
+    assert idx.k == 9
+    # the 10k exact reads all hit
+    assert (got[:, 1] > got[:, 0]).sum() >= 10_000 * 0.99
+    # same result through the fixed-length path and the host-buffer pipeline
+    got_fixed = gpu_match(idx, words, None, fixed_len=32)
+    assert np.array_equal(got, got_fixed)
+    assert np.array_equal(idx.match_host(words, lens, chunk=3000), got)
+
+
+def test_c2_full_parity():
+    c = synth.CONFIGS["C2"]
+    ref = c.reference()
+    words, lens = c.reads(ref)
+    check_full(ref.tobytes(), words=words, lens=lens)
+
+
+def test_repeat_rich_parity_small():
+    ref = synth.reference(synth.REF_REPEAT, 3_000_000, 33)
+    words, lens = synth.reads(ref, 200_000, 16, 160, 0.1, 0.01, 34)
+    check_full(ref.tobytes(), words=words, lens=lens)
+
+
+def test_locate_parity():
+    c = synth.CONFIGS["C2"]
+    ref = synth.reference(synth.REF_REPEAT, 500_000, 5)
+    words, lens = synth.reads(ref, 20_000, 8, 40, 0.1, 0.0, 6)
+    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens)
+    offs, pos = idx.locate(torch.from_numpy(got.view(np.int32)).cuda())
+    offs = offs.cpu().numpy()
+    pos = pos.cpu().numpy().view(np.uint32)
+    cnt = (got[:, 1].astype(np.int64) - got[:, 0])
+    assert np.array_equal(np.diff(offs), cnt) and offs[0] == 0
+    for q in range(0, 20_000, 97):
+        assert np.array_equal(pos[offs[q]:offs[q + 1]], oracle.locate(sa_ref, int(got[q, 0]), int(got[q, 1])))
+
+
+def _full_size_check(cfg, sample=2000, q_count=None):
+    ref = cfg.reference()
+    S = oracle.encode(ref)
+    idx = sa.Index(ref)
+    sa_gpu = idx.export_sa()
+    assert oracle.check_sa(S, sa_gpu) == -1, "GPU suffix array fails the oracle's SA check"
+    words, lens = cfg.reads(ref, q_count=q_count)
+    got = gpu_match(idx, words, None, fixed_len=cfg.m_max) if cfg.m_min == cfg.m_max else gpu_match(idx, words, lens)
+    # sampled outputs straight from the definition (no SA)
+    rng = np.random.default_rng(cfg.ref_seed)
+    qs = np.sort(rng.choice(words.shape[0], size=min(sample, words.shape[0]), replace=False))
+    want = oracle.count_batch(S, words[qs], lens[qs]).astype(np.uint32)
+    assert np.array_equal(got[qs], want)
+    # every query certified against the (verified) suffix array
+    nbad, first = oracle.certificate(S, sa_gpu, words, got, lens)
+    assert nbad == 0, f"{nbad} queries fail the certificate, first {first}"
+    return idx
+
+
+@pytest.mark.slow
+def test_c3_full_size():
+    _full_size_check(synth.CONFIGS["C3"])
+
+
+@pytest.mark.slow
+def test_c4_full_size():
+    _full_size_check(synth.CONFIGS["C4"], sample=256)
