@@ -170,7 +170,8 @@ def run_reference_arm(args):
     S = oracle.encode(ref)
     log(f"reference generated+encoded in {time.time() - t0:.1f}s")
     cores = oracle.max_threads()
-    s = sample_size(cfg, cores, args.cpu_seconds)
+    # keep the whole --steps/--warmup run within a few minutes
+    s = sample_size(cfg, cores, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     times = []
     for it in range(args.warmup + args.steps):
         # each step: a fresh bounded sample of the same read stream
