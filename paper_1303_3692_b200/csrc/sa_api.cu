@@ -141,28 +141,37 @@ __device__ __forceinline__ uint64_t hash64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// Each thread issues `loads` loads in groups of 8 independent addresses (slots is a power of two,
+// so the address is one hash + mask); dependent = 1 chains every address on the previous value.
 template <int BYTES>
-__global__ void k_gather(const uint8_t *__restrict__ buf, uint64_t slots, uint32_t loads, int dependent,
+__global__ void k_gather(const uint8_t *__restrict__ buf, uint64_t slot_mask, uint32_t loads, int dependent,
                          uint64_t *__restrict__ sink) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t acc = 0;
-    uint64_t h = hash64(tid + 0x1234567ull);
-#pragma unroll 8
-    for (uint32_t i = 0; i < loads; ++i) {
-        const uint64_t slot = (dependent ? (h ^ acc) : hash64(h + i)) % slots;
-        const uint8_t *p = buf + slot * BYTES;
-        if constexpr (BYTES == 32) {
-            const ulonglong4 v = *reinterpret_cast<const ulonglong4 *>(p);  // 256-bit load (sm_100)
-            acc += v.x ^ v.y ^ v.z ^ v.w;
-        } else if constexpr (BYTES == 16) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
-            acc += (uint64_t)v.x ^ v.y ^ v.z ^ v.w;
-        } else if constexpr (BYTES == 8) {
-            acc += __ldg(reinterpret_cast<const unsigned long long *>(p));
-        } else {
-            acc += __ldg(reinterpret_cast<const unsigned int *>(p));
+    uint64_t h = hash64(tid * 0x9E3779B97F4A7C15ull + 0x1234567ull);
+    for (uint32_t i = 0; i < loads; i += 8) {
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint64_t slot = (dependent ? hash64(h + acc + u) : hash64(h + i + u)) & slot_mask;
+            const uint8_t *p = buf + slot * BYTES;
+            if constexpr (BYTES == 32) {
+                const ulonglong4 x = *reinterpret_cast<const ulonglong4 *>(p);  // 256-bit load (sm_100)
+                v[u] = x.x ^ x.y ^ x.z ^ x.w;
+            } else if constexpr (BYTES == 16) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p));
+                v[u] = (uint64_t)x.x ^ x.y ^ x.z ^ x.w;
+            } else if constexpr (BYTES == 8) {
+                v[u] = __ldg(reinterpret_cast<const unsigned long long *>(p));
+            } else {
+                v[u] = __ldg(reinterpret_cast<const unsigned int *>(p));
+            }
+            if (dependent) acc += v[u];
         }
-        if (dependent) h = hash64(h + acc);
+        if (!dependent) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
+        }
     }
     if (acc == 0x5eed) sink[0] = acc;  // keeps the loads alive
 }
@@ -184,15 +193,16 @@ extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    const uint64_t slots = buffer_bytes / access_bytes;
+    uint64_t slots = 1;
+    while (slots * 2 * access_bytes <= buffer_bytes) slots *= 2;  // power of two: address = hash & mask
     const unsigned threads = 256;
     const unsigned blocks = (unsigned)((n_threads + threads - 1) / threads);
     auto launch = [&]() {
         switch (access_bytes) {
-        case 32: k_gather<32><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
-        case 16: k_gather<16><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
-        case 8: k_gather<8><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
-        default: k_gather<4><<<blocks, threads>>>(buf, slots, loads, dependent, sink); break;
+        case 32: k_gather<32><<<blocks, threads>>>(buf, slots - 1, loads, dependent, sink); break;
+        case 16: k_gather<16><<<blocks, threads>>>(buf, slots - 1, loads, dependent, sink); break;
+        case 8: k_gather<8><<<blocks, threads>>>(buf, slots - 1, loads, dependent, sink); break;
+        default: k_gather<4><<<blocks, threads>>>(buf, slots - 1, loads, dependent, sink); break;
         }
     };
     launch();  // warm-up
