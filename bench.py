@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--m", type=int, default=None, help="C5 read length (16..1000)")
     ap.add_argument("--q", type=int, default=None, help="override reads per GPU")
     ap.add_argument("--k", type=int, default=0, help="k-mer bracket k (0 = auto)")
+    ap.add_argument("--layout", default="records", choices=["records", "plain"],
+                    help="SA layout: 16-byte records caching 48 bases (default) or plain uint32 SA")
+    ap.add_argument("--simple", action="store_true", help="one read per thread (no lane refill), for A/B")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -135,15 +138,19 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def algorithmic_bytes_per_query(n, k, m):
-    """sector-granular bytes the k-mer-bracket joint search must move per query.
+def algorithmic_bytes_per_query(n, k, m, layout="records"):
+    """sector-granular bytes the k-mer-bracket joint search must move per read.
 
-    1 table sector (32 B) + D steps x (SA sector + text sector, 32 B each) + the packed read (m/4 B,
-    streamed) + the {lo, hi} result (8 B); D = log2(mean bracket + 1) + 1 (the joint lo/hi search:
-    one descent plus on average one extra level for the hi continuation)."""
+    D = log2(mean bracket + 1) + 1 search steps (the joint lo/hi search: one descent plus on average
+    one extra level for the hi continuation).
+      plain   : 1 table sector + D x (SA sector + text sector) + read (m/4 B) + result (8 B)
+      records : 1 table sector + D x (record sector) + 1 text sector (verifying the bases past the
+                48 cached ones) + read + result."""
     bracket = n / float(4 ** k)
     D = math.log2(bracket + 1.0) + 1.0
-    return 32.0 + D * 64.0 + math.ceil(m / 4.0) + 8.0
+    if layout == "plain":
+        return 32.0 + D * 64.0 + math.ceil(m / 4.0) + 8.0
+    return 32.0 + D * 32.0 + 32.0 + math.ceil(m / 4.0) + 8.0
 
 
 def traffic_per_launch(workload_name):
@@ -228,6 +235,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1303_3692_b200 as sa
+    from paper_1303_3692_b200 import shard
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -245,7 +253,7 @@ def main():
     ref = cfg.reference()
     log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
     t0 = time.time()
-    idx = sa.Index(ref, k=args.k, device=local)
+    idx = sa.Index(ref, k=args.k, device=local, plain=(args.layout == "plain"))
     torch.cuda.synchronize()
     log(f"index built in {time.time() - t0:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
     t0 = time.time()
@@ -254,7 +262,8 @@ def main():
     fixed = cfg.m_max if cfg.m_min == cfg.m_max else None
     words_h = torch.empty((Q, stride), dtype=torch.int64, pin_memory=True)
     lens_h = torch.empty(Q, dtype=torch.int32, pin_memory=True)
-    cfg.reads(ref, q_begin=rank * Q, words_out=words_h.numpy().view(np.uint64),
+    q_begin, _ = shard.shard(rank, world, Q)
+    cfg.reads(ref, q_begin=q_begin, words_out=words_h.numpy().view(np.uint64),
               lens_out=lens_h.numpy().view(np.uint32))
     words = words_h.to(dev, non_blocking=True)
     lens = None if fixed else lens_h.to(dev, non_blocking=True)
@@ -265,7 +274,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream)
+        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, simple=args.simple)
 
     for _ in range(args.warmup):
         step()
@@ -291,22 +300,9 @@ def main():
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
-    if world > 1:
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
-
+    elapsed_ms = shard.max_over_ranks(elapsed_ms, dev)
     # per-shard summary gathered over NCCL (the only collective): hits, sum of counts, checksum
-    res = out.view(torch.int64)  # (lo | hi<<32) per read, for a cheap checksum
-    lo = out[:, 0].to(torch.int64) & 0xFFFFFFFF
-    hi = out[:, 1].to(torch.int64) & 0xFFFFFFFF
-    summary = torch.stack([(hi > lo).sum(), (hi - lo).sum(), (res * 0x9E3779B1).sum()]).to(torch.int64)
-    if world > 1:
-        allsum = [torch.empty_like(summary) for _ in range(world)]
-        dist.all_gather(allsum, summary)
-        summary_all = torch.stack(allsum).cpu().tolist()
-    else:
-        summary_all = [summary.cpu().tolist()]
+    summary_all = shard.gather_summaries(shard.summarize(out))
 
     total_reads = Q * world * args.steps
     value = total_reads / (elapsed_ms * 1e-3)
@@ -314,7 +310,7 @@ def main():
 
     # ---- roofline of the dominant (only) kernel: k_match ----
     m_alg = cfg.m_max if fixed else (cfg.m_min + cfg.m_max) / 2
-    bpq = algorithmic_bytes_per_query(cfg.n, idx.k, m_alg)
+    bpq = algorithmic_bytes_per_query(cfg.n, idx.k, m_alg, args.layout)
     avg_launch_s = statistics.mean(launch_ms) * 1e-3
     achieved = bpq * Q / avg_launch_s / 1e9
     peak, peak_src = measured_peaks()
@@ -328,7 +324,22 @@ def main():
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
             "roofline": roofline, "clocks": sampler.result(), "gpu_launches": args.steps,
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
-            "shards": summary_all}
+            "shards": summary_all, "layout": args.layout, "kernel_mode": "simple" if args.simple else "lane-refill",
+            "index_bytes": idx.device_bytes}
+
+    # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
+    st = torch.empty(Q, dtype=torch.int32, device=dev)
+    chk = torch.empty_like(out)
+    idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, stats=st)
+    torch.cuda.synchronize()
+    if not torch.equal(chk, out):
+        raise RuntimeError("instrumented launch disagrees with the timed launches")
+    stv = st.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    steps_t, texts_t = (stv & 0xFFFF).double(), (stv >> 16).double()
+    line["search_stats"] = {"mean_steps": float(steps_t.mean()), "mean_text_windows": float(texts_t.mean()),
+                            "p99_steps": float(torch.quantile(steps_t[:1 << 20], 0.99)),
+                            "max_steps": float(steps_t.max())}
+    del st, chk
 
     # ---- random-gather microbenchmark (context for the roofline; untimed) ----
     if rank == 0:
@@ -353,10 +364,7 @@ def main():
         for _ in range(e2e_steps):
             idx.match_host(wn, ln, fixed_len=fixed, out=on)
         dt = time.perf_counter() - t
-        if world > 1:
-            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+        dt = shard.max_over_ranks(dt, dev)
         if not np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32)):
             raise RuntimeError("host-buffer path disagrees with the device path")
         line["e2e"] = {"value": Q * world * e2e_steps / dt, "unit": UNIT,

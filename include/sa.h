@@ -64,9 +64,21 @@ typedef enum {
 typedef struct {
     int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device */
     uint32_t kmer_k;   /* k of the k-mer bracket table, 1..16; 0 = auto (min(12, floor(log4 n))) */
-    uint32_t flags;    /* reserved, must be 0 */
+    uint32_t flags;    /* 0 or SA_INDEX_PLAIN */
     uint32_t reserved; /* must be 0 */
 } sa_index_opts;
+
+/* sa_index_opts.flags.  Default layout: the suffix array is stored as 16-byte records
+ * {SA[r], the 48 bases of suffix SA[r] that follow its first k bases} so that one 32-byte
+ * sector per search step decides most comparisons (16 B x n of HBM).  SA_INDEX_PLAIN keeps a
+ * plain uint32 SA (4 B x n) and reads the packed text at every step. */
+#define SA_INDEX_PLAIN 1u
+
+/* sa_match_batch flags. */
+#define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace:
+                              uint32 per query = steps | (text windows fetched << 16); the
+                              workspace must then hold >= 4*Q bytes */
+#define SA_MATCH_SIMPLE 2u /* one query per thread, no lane refill (for A/B measurement) */
 
 /* Build the index of ref_ascii[0..n) (host memory, case-insensitive ACGT) on
  * the device: validate + pack to 2 bits/base, build the suffix array on the
@@ -99,10 +111,11 @@ sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
  *   q_len     dev, Q uint32 lengths, or NULL: every query has fixed_len bases.
  *   out_lohi  dev, 2Q uint32: out_lohi[2q] = lo, out_lohi[2q+1] = hi
  *             (Alg. 1 lines 44-45, res[thd<<1] = LB, res[(thd<<1)+1] = RB, reading A8).
- *   workspace dev scratch of sa_match_workspace_size() bytes (may be NULL if that is 0).
- *   flags     0 (reserved).
- * Requirements: every length m <= 32*stride_words and m <= 65535.  Q == 0 is a
- * no-op.  Errors: SA_EINVAL.  Asynchronous on `stream`. */
+ *   workspace dev scratch of sa_match_workspace_size() bytes (may be NULL if that is 0;
+ *             >= 4*Q bytes with SA_MATCH_STATS).
+ *   flags     0, or SA_MATCH_STATS / SA_MATCH_SIMPLE (above).
+ * Requirements: every length m <= 32*stride_words (longer lengths are clamped) and
+ * m <= 65535.  Q == 0 is a no-op.  Errors: SA_EINVAL.  Asynchronous on `stream`. */
 sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, size_t *bytes);
 sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                          uint32_t stride_words, uint64_t Q, uint32_t *out_lohi, void *workspace, size_t ws_bytes,

@@ -20,6 +20,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsa.so")
 
 SA_OK, SA_EINVAL, SA_ESYMBOL, SA_ETOOLONG, SA_ENOMEM, SA_ECUDA, SA_EEMPTY = 0, -1, -2, -3, -4, -5, -6
+SA_INDEX_PLAIN = 1          # sa_index_opts.flags: plain uint32 SA instead of 16-byte records
+SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windows << 16 into the workspace
+SA_MATCH_SIMPLE = 2         # sa_match_batch flags: one query per thread (no lane refill)
 _NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
           -6: "SA_EEMPTY"}
 
@@ -98,14 +101,16 @@ class Index:
     """Suffix-array index of one reference on one GPU (``sa_index_create``).
 
     ref: str / bytes / numpy uint8 array of ACGT (case-insensitive).  k: bracket-table k (0 = auto).
+    plain: keep a plain uint32 SA (SA_INDEX_PLAIN) instead of the default 16-byte records.
     """
 
-    def __init__(self, ref, k: int = 0, device: Optional[int] = None):
+    def __init__(self, ref, k: int = 0, device: Optional[int] = None, plain: bool = False):
         if isinstance(ref, str):
             ref = ref.encode("ascii")
         arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
             np.ascontiguousarray(ref, dtype=np.uint8)
-        opts = _Opts(-1 if device is None else int(device), int(k), 0, 0)
+        opts = _Opts(-1 if device is None else int(device), int(k), SA_INDEX_PLAIN if plain else 0, 0)
+        self.plain = bool(plain)
         h = _p()
         _check(lib().sa_index_create(arr.ctypes.data if arr.size else None, arr.size, ctypes.byref(opts),
                                      ctypes.byref(h)), "sa_index_create")
@@ -150,11 +155,14 @@ class Index:
         return out
 
     # ---- the hot path ----
-    def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None):
+    def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, stats=None,
+              simple: bool = False):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
         lens:  CUDA int32 tensor [Q] (uint32 lengths) or None with fixed_len.
+        stats: optional CUDA int32 tensor [Q] -> per-query steps | text windows << 16 (SA_MATCH_STATS).
+        simple: one query per thread (SA_MATCH_SIMPLE, for A/B measurement).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi); view it as uint32 on the host.
         """
         import torch
@@ -167,8 +175,12 @@ class Index:
         if out is None:
             out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
+        flags = (SA_MATCH_SIMPLE if simple else 0) | (SA_MATCH_STATS if stats is not None else 0)
+        if stats is not None:
+            assert stats.is_cuda and stats.numel() >= Q and stats.element_size() == 4
         _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(out),
-                                    None, 0, 0, _stream_ptr(stream)), "sa_match_batch")
+                                    _dptr(stats), 0 if stats is None else 4 * Q, flags, _stream_ptr(stream)),
+               "sa_match_batch")
         return out
 
     def match_host(self, words: np.ndarray, lens: Optional[np.ndarray] = None, fixed_len: Optional[int] = None,

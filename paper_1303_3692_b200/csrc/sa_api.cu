@@ -26,6 +26,7 @@ static void free_index(sa_index *idx) {
     cudaDeviceSynchronize();
     cudaFree(idx->text);
     cudaFree(idx->sa);
+    cudaFree(idx->rec);
     cudaFree(idx->table);
     for (int b = 0; b < 2; ++b) {
         cudaFree(idx->pipe_words[b]);
@@ -50,7 +51,10 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     }
     sa_index_opts o{-1, 0, 0, 0};
     if (opts) o = *opts;
-    if (o.flags != 0 || o.reserved != 0) { sa_set_error("opts.flags/reserved must be 0"); return SA_EINVAL; }
+    if ((o.flags & ~SA_INDEX_PLAIN) != 0 || o.reserved != 0) {
+        sa_set_error("unknown opts.flags bits / reserved must be 0");
+        return SA_EINVAL;
+    }
     if (o.kmer_k > 16) { sa_set_error("kmer_k %u out of range 1..16", o.kmer_k); return SA_EINVAL; }
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -70,6 +74,7 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     if (!idx) { sa_set_error("host allocation failed"); cudaSetDevice(prev); return SA_ENOMEM; }
     idx->device = dev;
     idx->n = n;
+    idx->plain = (o.flags & SA_INDEX_PLAIN) != 0;
     uint32_t k = o.kmer_k;
     if (k == 0) {  // auto: floor(log4 n), at most 12 (a 64 MiB table)
         k = 1;
@@ -120,7 +125,9 @@ static sa_status export_copy(const sa_index *idx, void *dst, const void *src, si
 
 extern "C" sa_status sa_index_export_sa(const sa_index *idx, uint32_t *host_out) {
     sa_clear_error();
-    return export_copy(idx, host_out, idx ? idx->sa : nullptr, idx ? idx->n * sizeof(uint32_t) : 0);
+    if (!idx || !host_out) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    return sa_extract_sa(idx, host_out);
 }
 
 extern "C" sa_status sa_index_export_table(const sa_index *idx, uint32_t *host_out) {

@@ -288,12 +288,45 @@ sa_status build_sa(sa_index *idx, cudaStream_t st) {
     return SA_OK;
 }
 
+// SA records: {SA[r], bases k+32..k+47 of the suffix, bases k..k+31 (lo word, hi word)}; bases past n are 0.
+__global__ void k_records(const uint64_t *__restrict__ text, uint64_t n, unsigned k, const uint32_t *__restrict__ sa,
+                          uint4 *__restrict__ rec) {
+    GRID_STRIDE(r, n) {
+        const uint64_t s = sa[r];
+        const uint64_t c01 = text_window(text, s + k);
+        const uint64_t c2 = text_window(text, s + k + 32) >> 32;
+        rec[r] = make_uint4((uint32_t)s, (uint32_t)c2, (uint32_t)c01, (uint32_t)(c01 >> 32));
+    }
+}
+
+__global__ void k_extract_sa(const uint4 *__restrict__ rec, uint64_t count, uint32_t *__restrict__ out) {
+    GRID_STRIDE(r, count) { out[r] = rec[r].x; }
+}
+
 }  // namespace
+
+sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out) {
+    const uint64_t n = idx->n;
+    if (idx->plain) {
+        SA_CUDA_TRY(cudaMemcpy(host_out, idx->sa, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        return SA_OK;
+    }
+    const uint64_t CH = 1ull << 28;
+    DevBuf<uint32_t> tmp;
+    SA_TRY(tmp.alloc(n < CH ? n : CH, nullptr, "SA export staging"));
+    for (uint64_t off = 0; off < n; off += CH) {
+        const uint64_t c = (n - off < CH) ? n - off : CH;
+        k_extract_sa<<<grid_for(c), kThreads>>>(idx->rec + off, c, tmp.p);
+        SA_CUDA_TRY(cudaGetLastError());
+        SA_CUDA_TRY(cudaMemcpy(host_out + off, tmp.p, c * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    }
+    return SA_OK;
+}
 
 sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) {
     const uint64_t n = idx->n;
     // ---- 1. upload + validate + pack (chunks of 256 MiB) ----
-    idx->n_words = (n + 31) / 32 + 2;
+    idx->n_words = (n + 31) / 32 + kGuardWords;
     SA_CUDA_TRY(cudaMalloc(&idx->text, idx->n_words * sizeof(uint64_t)));
     SA_CUDA_TRY(cudaMemsetAsync(idx->text, 0, idx->n_words * sizeof(uint64_t), st));
     {
@@ -327,8 +360,22 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
     SA_CUDA_TRY(cudaMalloc(&idx->table, (K + 1) * sizeof(uint32_t)));
     k_table<<<grid_for(n + 1), kThreads, 0, st>>>(idx->text, n, idx->sa, idx->k, idx->table);
     SA_CUDA_TRY(cudaGetLastError());
+    // ---- 4. SA records (default layout) ----
+    uint64_t sa_bytes = n * sizeof(uint32_t);
+    if (!idx->plain) {
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        SA_CUDA_TRY(cudaMalloc(&idx->rec, n * sizeof(uint4)));
+        k_records<<<grid_for(n), kThreads, 0, st>>>(idx->text, n, idx->k, idx->sa, idx->rec);
+        SA_CUDA_TRY(cudaGetLastError());
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_CUDA_TRY(cudaFree(idx->sa));
+        idx->sa = nullptr;
+        sa_bytes = n * sizeof(uint4);
+    }
     SA_CUDA_TRY(cudaStreamSynchronize(st));
-    idx->device_bytes = idx->n_words * 8 + n * 4 + (K + 1) * 4;
+    idx->device_bytes = idx->n_words * 8 + sa_bytes + (K + 1) * 4;
     // hand the build's transient memory back to the driver
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);

@@ -70,13 +70,23 @@ struct DevBuf {
 
 // ---------------------------------------------------------------------------------------------
 // the index (immutable after create)
+constexpr uint64_t kGuardWords = 4;  // zero words past the text: windows up to base n + 95 are readable
+constexpr uint32_t kCacheBases = 48; // bases cached per SA record (after the first k)
+
+// SA values of the layout: base pointer + stride in uint32 units
+struct SaView {
+    const uint32_t *base;
+    uint32_t stride;
+};
 struct sa_index {
     int device = 0;
     uint64_t n = 0;          // reference length
     uint32_t k = 0;          // k-mer bracket table
-    uint64_t n_words = 0;    // packed text words incl. 2 zero guard words
-    uint64_t *text = nullptr;    // dev: 2-bit MSB-first, zero-padded past n
-    uint32_t *sa = nullptr;      // dev: n entries
+    uint64_t n_words = 0;    // packed text words incl. kGuardWords zero guard words
+    uint64_t *text = nullptr;    // dev: 2-bit MSB-first, zero-padded past n (kGuardWords zero words)
+    bool plain = false;          // SA_INDEX_PLAIN: sa[] only; else rec[] only
+    uint32_t *sa = nullptr;      // dev: n entries (plain layout)
+    uint4 *rec = nullptr;        // dev: n records {SA[r], cache bases k+32..k+47, cache bases k..k+31 (lo, hi)}
     uint32_t *table = nullptr;   // dev: 4^k + 1 entries
     uint64_t device_bytes = 0;
     uint32_t build_rounds = 0;   // prefix-doubling rounds after the initial sort
@@ -107,5 +117,10 @@ __device__ __forceinline__ uint64_t prefix_mask(unsigned L) {
     return L >= 32 ? ~0ull : (L == 0 ? 0ull : ~(~0ull >> (2u * L)));
 }
 
+inline SaView sa_view(const sa_index *idx) {
+    return idx->plain ? SaView{idx->sa, 1u} : SaView{reinterpret_cast<const uint32_t *>(idx->rec), 4u};
+}
+
 // build / match entry points implemented in sa_build.cu / sa_match.cu
 sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st);
+sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out);

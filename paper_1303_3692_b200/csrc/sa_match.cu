@@ -24,7 +24,8 @@ namespace {
 
 struct MatchArgs {
     const uint64_t *__restrict__ text;
-    const uint32_t *__restrict__ sa;
+    const uint32_t *__restrict__ sa;   // plain layout
+    const uint4 *__restrict__ rec;     // record layout
     const uint32_t *__restrict__ table;
     uint64_t n;
     uint32_t k;
@@ -34,6 +35,7 @@ struct MatchArgs {
     uint32_t stride;
     uint64_t Q;
     uint32_t *__restrict__ out;
+    uint32_t *__restrict__ stats;      // SA_MATCH_STATS
 };
 
 // Query words: QW > 0 -> registers (fully unrolled so indices are static); QW == 0 -> global.
@@ -45,12 +47,17 @@ struct QueryWords {
         for (int j = 0; j < QW; ++j) w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
     }
     __device__ __forceinline__ uint64_t first() const { return w[0]; }
+    __device__ __forceinline__ uint64_t word(int j) const { return j < QW ? w[j] : 0ull; }
 };
 template <>
 struct QueryWords<0> {
     const uint64_t *p;
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t) { p = q; }
+    uint32_t nw;
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n) { p = q; nw = n; }
     __device__ __forceinline__ uint64_t first() const { return __ldg(reinterpret_cast<const unsigned long long *>(p)); }
+    __device__ __forceinline__ uint64_t word(int j) const {
+        return (uint32_t)j < nw ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+    }
 };
 
 // One 32-base step of the compare: word j of P against the text at s + 32j.
@@ -104,81 +111,193 @@ __device__ __forceinline__ void compare(const uint64_t *__restrict__ text, uint6
     lcp = m;
 }
 
-// Binary search over (L, R) for the boundary where `P <= t` (lower = true, Alg. 1 LB loop) or
-// `P < t` (lower = false, RB loop) starts; returns R.
+// Compare P (m >= k, inside its k-mer bracket) with the suffix of SA record r.  The record caches
+// the 48 bases after the first k, which every long suffix in the bracket shares with P; the text
+// is read only when those 48 bases are equal and more remain, or for the < k suffixes shorter
+// than k (which can sit at the end of a bracket without sharing its k-mer).
 template <int QW>
-__device__ __forceinline__ int64_t bound(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, int64_t L,
-                                         int64_t R, uint32_t lcpL, uint32_t lcpR, bool lower) {
-    while (R - L > 1) {
-        const int64_t p = (L + R) >> 1;
-        const uint64_t s = __ldg(a.sa + p);
-        int sign;
-        uint32_t lcp;
-        compare<QW>(a.text, a.n, s, P, m, min(lcpL, lcpR), sign, lcp);
-        const bool go_left = lower ? (sign <= 0) : (sign < 0);
-        if (go_left) { R = p; lcpR = lcp; } else { L = p; lcpL = lcp; }
+__device__ __forceinline__ void rec_compare(const uint64_t *__restrict__ text, uint64_t n, uint32_t k, const uint4 r,
+                                            const QueryWords<QW> &P, uint64_t pk01, uint32_t pk2, uint32_t m,
+                                            uint32_t skip, int &sign, uint32_t &lcp, uint32_t &texts) {
+    const uint64_t s = r.x;
+    const uint64_t len = n - s;
+    if (len < k || skip >= k + kCacheBases) {
+        ++texts;
+        compare<QW>(text, n, s, P, m, len < k ? 0u : skip, sign, lcp);
+        return;
     }
-    return R;
+    const uint32_t avail = (uint32_t)((m < len ? (uint64_t)m : len) - k);  // bases after k present in both
+    const uint64_t c01 = ((uint64_t)r.w << 32) | r.z;
+    const uint64_t mask1 = prefix_mask(min(32u, avail));
+    const uint64_t a1 = pk01 & mask1, b1 = c01 & mask1;
+    if (a1 != b1) {
+        lcp = k + ((uint32_t)__clzll((long long)(a1 ^ b1)) >> 1);
+        sign = a1 > b1 ? 1 : -1;
+        return;
+    }
+    if (avail > 32) {
+        const uint32_t L2 = min(16u, avail - 32);
+        const uint32_t mask2 = L2 >= 16 ? ~0u : ~(~0u >> (2 * L2));
+        const uint32_t a2 = pk2 & mask2, b2 = r.y & mask2;
+        if (a2 != b2) {
+            lcp = k + 32 + ((uint32_t)__clz((int)(a2 ^ b2)) >> 1);
+            sign = a2 > b2 ? 1 : -1;
+            return;
+        }
+        if (avail > kCacheBases) {
+            ++texts;
+            compare<QW>(text, n, s, P, m, k + kCacheBases, sign, lcp);
+            return;
+        }
+    }
+    // every base present in both is equal
+    if (m <= len) { sign = 0; lcp = m; }            // P is a prefix of the suffix (case 1)
+    else { sign = 1; lcp = (uint32_t)len; }          // the suffix is a proper prefix of P (reading A7)
 }
 
-template <int QW>
+enum : int { M_IDLE = 0, M_JOINT, M_HI, M_SHORT_LO, M_SHORT_HI };
+
+// The search as a per-lane state machine.  Each loop iteration performs ONE binary-search step
+// for whatever query the lane currently holds; a lane whose query is finished writes {lo, hi} and
+// immediately takes its next query (grid-stride), so lanes of a warp stay busy even though reads
+// need very different numbers of steps (repeats: up to ~32, unique reads: ~9).
+//   M_JOINT     LB rule (R moves when P <= t) over the k-mer bracket, remembering the first pivot
+//               where P is a prefix of the suffix (the split);
+//   M_HI        RB rule (R moves when P < t) over (split, R at the split);
+//   M_SHORT_*   m < k: LB then RB rule over the two small windows below T[xa] and T[xb].
+// L is kept as L+1 (Lp1) so every bound fits uint32.
+template <int QW, bool REC, bool STATS>
 __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
-    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= a.Q) return;
-    // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
-    const uint32_t m = min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
-    const uint32_t nw = (m + 31) >> 5;
-    QueryWords<QW> P;
-    P.load(a.words + q * a.stride, nw);
-    int64_t lo, hi;
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t k = a.k;
-    if (m == 0) {  // the empty query is a prefix of every suffix (reading A12)
-        lo = 0;
-        hi = (int64_t)a.n;
-    } else if (m >= k) {
-        // all suffixes before T[x] are < P, all from T[x+1] on are > P
-        const uint64_t x = P.first() >> (64 - 2 * k);
-        int64_t L = (int64_t)__ldg(a.table + x) - 1;
-        int64_t R = (int64_t)__ldg(a.table + x + 1);
-        uint32_t lcpL = 0, lcpR = 0;
-        int64_t sL = -2, sR = 0;  // split: first pivot with P a prefix of its suffix
-        uint32_t slcpR = 0;
-        while (R - L > 1) {
-            const int64_t p = (L + R) >> 1;
-            const uint64_t s = __ldg(a.sa + p);
-            int sign;
-            uint32_t lcp;
-            compare<QW>(a.text, a.n, s, P, m, min(lcpL, lcpR), sign, lcp);
-            if (sign > 0) {
-                L = p;
-                lcpL = lcp;
+    QueryWords<QW> P;
+    uint64_t pk01 = 0;
+    uint32_t pk2 = 0, m = 0;
+    uint32_t Lp1 = 0, R = 0, lcpL = 0, lcpR = 0;
+    uint32_t sLp1 = 0, sR = 0, slcpR = 0, lo = 0;
+    uint32_t nsteps = 0, ntexts = 0;
+    int mode = M_IDLE;
+    bool split = false, first = true;
+    for (;;) {
+        if (mode == M_IDLE) {
+            if (!first) q += nthreads;
+            first = false;
+            if (q >= a.Q) break;
+            // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
+            m = min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
+            P.load(a.words + q * a.stride, (m + 31) >> 5);
+            nsteps = ntexts = 0;
+            lcpL = lcpR = 0;
+            if (m == 0) {  // the empty query is a prefix of every suffix (reading A12)
+                lo = 0;
+                Lp1 = R = (uint32_t)a.n;
+                mode = M_HI;
+            } else if (m >= k) {
+                // all suffixes before T[x] are < P, all from T[x+1] on are > P
+                const uint64_t x = P.first() >> (64 - 2 * k);
+                Lp1 = __ldg(a.table + x);
+                R = __ldg(a.table + x + 1);
+                split = false;
+                mode = M_JOINT;
+                if (REC) {
+                    const uint64_t w0 = P.word(0), w1 = P.word(1), w2 = P.word(2);
+                    pk01 = (w0 << (2 * k)) | (w1 >> (64 - 2 * k));
+                    pk2 = (uint32_t)(((w1 << (2 * k)) | (w2 >> (64 - 2 * k))) >> 32);
+                }
             } else {
-                if (sign == 0 && sL == -2) { sL = p; sR = R; slcpR = lcpR; }
-                R = p;
-                lcpR = lcp;
+                // m < k: lo in [T[xa]-(k-m), T[xa]], hi in [T[xb]-(k-1), T[xb]] with xa = x.a^(k-m),
+                // xb = (x+1).a^(k-m); searched over T[.]-k .. T[.]
+                const uint64_t x = P.first() >> (64 - 2 * m);
+                const uint32_t Ta = __ldg(a.table + (x << (2 * (k - m))));
+                const uint32_t Tb = __ldg(a.table + ((x + 1) << (2 * (k - m))));
+                Lp1 = Ta > k ? Ta - k : 0;
+                R = Ta;
+                sLp1 = Tb > k ? Tb - k : 0;
+                sR = Tb;
+                mode = M_SHORT_LO;
             }
         }
-        lo = R;
-        hi = (sL == -2) ? lo : bound<QW>(a, P, m, sL, sR, m, slcpR, false);
-    } else {
-        // m < k: lo lies in [T[xa]-k, T[xa]] and hi in [T[xb]-k, T[xb]], xa = x.a^(k-m),
-        // xb = (x+1).a^(k-m)
-        const uint64_t x = P.first() >> (64 - 2 * m);
-        const uint64_t xa = x << (2 * (k - m)), xb = (x + 1) << (2 * (k - m));
-        const int64_t Ta = (int64_t)__ldg(a.table + xa), Tb = (int64_t)__ldg(a.table + xb);
-        lo = bound<QW>(a, P, m, (Ta > (int64_t)k ? Ta - (int64_t)k : 0) - 1, Ta, 0, 0, true);
-        hi = bound<QW>(a, P, m, (Tb > (int64_t)k ? Tb - (int64_t)k : 0) - 1, Tb, 0, 0, false);
+        // finished intervals: move to the next phase or emit the result
+        while (mode != M_IDLE && R <= Lp1) {
+            if (mode == M_JOINT) {
+                lo = R;
+                if (split) {
+                    Lp1 = sLp1; R = sR; lcpL = m; lcpR = slcpR;
+                    mode = M_HI;
+                    continue;
+                }
+            } else if (mode == M_SHORT_LO) {
+                lo = R;
+                Lp1 = sLp1; R = sR; lcpL = lcpR = 0;
+                mode = M_SHORT_HI;
+                continue;
+            }
+            // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
+            const uint32_t hi = (mode == M_JOINT) ? lo : R;
+            reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+            if (STATS) a.stats[q] = nsteps | (ntexts << 16);
+            mode = M_IDLE;
+        }
+        if (mode == M_IDLE) continue;
+        // ---- one binary-search step ----
+        const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
+        int sign;
+        uint32_t lcp;
+        const uint32_t skip = min(lcpL, lcpR);
+        if constexpr (REC) {
+            const uint4 r = __ldg(a.rec + p);
+            if (mode <= M_HI) {
+                rec_compare<QW>(a.text, a.n, k, r, P, pk01, pk2, m, skip, sign, lcp, ntexts);
+            } else {
+                ++ntexts;
+                compare<QW>(a.text, a.n, r.x, P, m, skip, sign, lcp);
+            }
+        } else {
+            const uint64_t s = __ldg(a.sa + p);
+            ++ntexts;
+            compare<QW>(a.text, a.n, s, P, m, skip, sign, lcp);
+        }
+        ++nsteps;
+        if (mode == M_JOINT && sign == 0 && !split) {  // first pivot with P a prefix of its suffix
+            split = true;
+            sLp1 = p + 1;
+            sR = R;
+            slcpR = lcpR;
+        }
+        const bool go_left = sign < 0 || (sign == 0 && (mode == M_JOINT || mode == M_SHORT_LO));
+        if (go_left) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
     }
-    // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
-    reinterpret_cast<uint2 *>(a.out)[q] = make_uint2((uint32_t)lo, (uint32_t)hi);
+}
+
+template <int QW, bool REC, bool STATS>
+cudaError_t launch_match_t(const MatchArgs &a, bool simple, cudaStream_t st) {
+    const int threads = 256;
+    uint64_t blocks;
+    if (simple) {
+        blocks = (a.Q + threads - 1) / threads;  // one query per thread
+    } else {
+        static int per_sm[64] = {0};
+        static int sms[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && per_sm[dev] == 0) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k_match<QW, REC, STATS>, threads, 0);
+            cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+        }
+        const uint64_t resident = (uint64_t)(dev < 64 ? per_sm[dev] * sms[dev] : 148 * 4);
+        const uint64_t need = (a.Q + threads - 1) / threads;
+        blocks = need < resident ? need : resident;  // persistent: one wave, lanes refill
+    }
+    if (blocks == 0) blocks = 1;
+    k_match<QW, REC, STATS><<<(unsigned)blocks, threads, 0, st>>>(a);
+    return cudaGetLastError();
 }
 
 template <int QW>
-cudaError_t launch_match(const MatchArgs &a, cudaStream_t st) {
-    const int threads = 256;
-    const uint64_t blocks = (a.Q + threads - 1) / threads;
-    k_match<QW><<<(unsigned)blocks, threads, 0, st>>>(a);
-    return cudaGetLastError();
+cudaError_t launch_match_qw(const MatchArgs &a, bool rec, bool stats, bool simple, cudaStream_t st) {
+    if (rec) return stats ? launch_match_t<QW, true, true>(a, simple, st) : launch_match_t<QW, true, false>(a, simple, st);
+    return stats ? launch_match_t<QW, false, true>(a, simple, st) : launch_match_t<QW, false, false>(a, simple, st);
 }
 
 // ---- locate -----------------------------------------------------------------------------------
@@ -191,7 +310,8 @@ struct CountOp {
 };
 
 // One warp per query: lanes copy SA[lo .. hi) to positions[off ..] (contiguous, coalesced).
-__global__ void k_locate(const uint32_t *__restrict__ sa, const uint32_t *__restrict__ lohi,
+// SA values are read through the layout's view (stride 1 = plain SA, 4 = 16-byte records).
+__global__ void k_locate(const uint32_t *__restrict__ sa, uint32_t sa_stride, const uint32_t *__restrict__ lohi,
                          const uint64_t *__restrict__ offsets, uint64_t Q, uint32_t *__restrict__ pos) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -199,7 +319,7 @@ __global__ void k_locate(const uint32_t *__restrict__ sa, const uint32_t *__rest
     for (uint64_t q = warp; q < Q; q += nwarps) {
         const uint32_t lo = lohi[2 * q], hi = lohi[2 * q + 1];
         const uint64_t off = offsets[q];
-        for (uint64_t j = lane; j < (uint64_t)(hi - lo); j += 32) pos[off + j] = __ldg(sa + lo + j);
+        for (uint64_t j = lane; j < (uint64_t)(hi - lo); j += 32) pos[off + j] = __ldg(sa + (lo + j) * sa_stride);
     }
 }
 
@@ -225,15 +345,17 @@ extern "C" sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, ui
     if (!idx || !bytes) { sa_set_error("NULL argument"); return SA_EINVAL; }
     (void)Q;
     (void)stride_words;
-    *bytes = 0;
+    *bytes = 0;  // the match itself needs no scratch; SA_MATCH_STATS needs 4*Q bytes
     return SA_OK;
 }
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
-                              uint32_t stride, uint64_t Q, uint32_t *out, cudaStream_t st) {
+                              uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, bool simple,
+                              cudaStream_t st) {
     MatchArgs a;
     a.text = idx->text;
     a.sa = idx->sa;
+    a.rec = idx->rec;
     a.table = idx->table;
     a.n = idx->n;
     a.k = idx->k;
@@ -243,11 +365,13 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.stride = stride;
     a.Q = Q;
     a.out = out;
+    a.stats = stats;
+    const bool rec = !idx->plain, st_on = stats != nullptr;
     cudaError_t e;
-    if (stride <= 1) e = launch_match<1>(a, st);
-    else if (stride <= 2) e = launch_match<2>(a, st);
-    else if (stride <= 4) e = launch_match<4>(a, st);
-    else e = launch_match<0>(a, st);
+    if (stride <= 1) e = launch_match_qw<1>(a, rec, st_on, simple, st);
+    else if (stride <= 2) e = launch_match_qw<2>(a, rec, st_on, simple, st);
+    else if (stride <= 4) e = launch_match_qw<4>(a, rec, st_on, simple, st);
+    else e = launch_match_qw<0>(a, rec, st_on, simple, st);
     if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
     return SA_OK;
 }
@@ -256,13 +380,20 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
                                     uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t *out_lohi,
                                     void *workspace, size_t ws_bytes, uint32_t flags, void *stream) {
     sa_clear_error();
-    (void)workspace;
-    (void)ws_bytes;
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
-    if (flags != 0) { sa_set_error("flags must be 0"); return SA_EINVAL; }
+    if (flags & ~(SA_MATCH_STATS | SA_MATCH_SIMPLE)) { sa_set_error("unknown flags 0x%x", flags); return SA_EINVAL; }
+    uint32_t *stats = nullptr;
+    if (flags & SA_MATCH_STATS) {
+        if (!workspace || ws_bytes < Q * sizeof(uint32_t)) {
+            sa_set_error("SA_MATCH_STATS needs a workspace of >= 4*Q bytes");
+            return SA_EINVAL;
+        }
+        stats = static_cast<uint32_t *>(workspace);
+    }
     if (Q == 0) return SA_OK;
     SA_CUDA_TRY(cudaSetDevice(idx->device));
-    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, (cudaStream_t)stream);
+    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats,
+                        (flags & SA_MATCH_SIMPLE) != 0, (cudaStream_t)stream);
 }
 
 extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
@@ -307,7 +438,7 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], st));
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, false, st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }
@@ -357,7 +488,8 @@ extern "C" sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, co
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     uint64_t blocks = (Q * 32 + 255) / 256;
     if (blocks > 148ull * 32) blocks = 148ull * 32;
-    k_locate<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(idx->sa, out_lohi, offsets, Q, positions);
+    const SaView v = sa_view(idx);
+    k_locate<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(v.base, v.stride, out_lohi, offsets, Q, positions);
     SA_CUDA_TRY(cudaGetLastError());
     return SA_OK;
 }

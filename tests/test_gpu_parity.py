@@ -25,18 +25,21 @@ def _text(s):
     return s.encode("ascii") if isinstance(s, str) else s
 
 
-def gpu_match(idx, words, lens=None, fixed_len=None):
+def gpu_match(idx, words, lens=None, fixed_len=None, simple=False, stats=None):
     w = torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).cuda()
     l = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).cuda()
-    out = idx.match(w, l, fixed_len=fixed_len)
+    out = idx.match(w, l, fixed_len=fixed_len, simple=simple, stats=stats)
     torch.cuda.synchronize()
     return out.cpu().numpy().view(np.uint32)
 
 
-def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True):
+LAYOUTS = [False, True]  # records (default), plain SA
+
+
+def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, plain=False):
     """Build on the GPU; compare SA, table and every interval with the oracle."""
     S = oracle.encode(text_ascii)
-    idx = sa.Index(text_ascii, k=k)
+    idx = sa.Index(text_ascii, k=k, plain=plain)
     sa_ref = oracle.sa_naive(S)
     if check_sa:
         assert np.array_equal(idx.export_sa(), sa_ref)
@@ -44,10 +47,12 @@ def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=Tr
         assert np.array_equal(idx.export_table(), oracle.kmer_table(S, idx.k))
     if queries is not None:
         words, lens = synth.pack_strings(queries)
-    got = gpu_match(idx, words, lens)
     want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
-    bad = np.nonzero((got != want).any(axis=1))[0]
-    assert bad.size == 0, f"{bad.size} mismatches, first q={bad[0]}: got {got[bad[0]]} want {want[bad[0]]}"
+    for simple in (False, True):
+        got = gpu_match(idx, words, lens, simple=simple)
+        bad = np.nonzero((got != want).any(axis=1))[0]
+        assert bad.size == 0, f"{bad.size} mismatches (simple={simple}), first q={bad[0]}: got {got[bad[0]]} " \
+                              f"want {want[bad[0]]}"
     return idx, S, sa_ref, got
 
 
@@ -94,12 +99,13 @@ def test_paper_example_table1_and_sec4():
 
 # ---- small adversarial texts: SA, table and intervals bit-exact --------------------------------
 
+@pytest.mark.parametrize("plain", LAYOUTS)
 @pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 63, 64, 65, 1000, 4097])
-@pytest.mark.parametrize("k", [0, 1, 3, 6])
-def test_random_texts_all_k(n, k):
+@pytest.mark.parametrize("k", [0, 1, 3, 6, 16])
+def test_random_texts_all_k(n, k, plain):
     rng = random.Random(n * 10 + k)
     text = "".join(rng.choice("ACGT") for _ in range(n))
-    check_full(text, hazard_queries(text, k or 6, rng), k=k)
+    check_full(text, hazard_queries(text, k or 6, rng), k=k, plain=plain)
 
 
 @pytest.mark.parametrize("text", [
@@ -109,9 +115,10 @@ def test_random_texts_all_k(n, k):
     "T" * 777 + "A" * 333,
     "ACGTTGCA" * 900,
 ])
-def test_periodic_and_homopolymer_texts(text):
+@pytest.mark.parametrize("plain", LAYOUTS)
+def test_periodic_and_homopolymer_texts(text, plain):
     rng = random.Random(len(text))
-    check_full(text, hazard_queries(text, 8, rng), k=8)
+    check_full(text, hazard_queries(text, 8, rng), k=8, plain=plain)
 
 
 def test_homopolymer_closed_form():
@@ -152,14 +159,37 @@ def test_de_bruijn_every_kmer_once():
     assert np.all(got[:, 1] - got[:, 0] == 1)
 
 
-def test_short_queries_below_k():
+@pytest.mark.parametrize("plain", LAYOUTS)
+def test_short_queries_below_k(plain):
     # m < k exercises the widened brackets
     rng = random.Random(7)
     for n in [20, 300, 5000]:
         text = "".join(rng.choice("AC") for _ in range(n)) + "".join(rng.choice("ACGT") for _ in range(n))
         qs = ["".join(p) for m in range(1, 5) for p in itertools.product("ACGT", repeat=m)]
         qs += [text[-j:] for j in range(1, 12)]
-        check_full(text, qs, k=10)
+        check_full(text, qs, k=10, plain=plain)
+
+
+def test_long_reads_generic_path():
+    # stride > 4 words: the generic (global-memory query) kernel, reads up to 1000 bp with long matches
+    ref = synth.reference(synth.REF_REPEAT, 400_000, 21)
+    for plain in LAYOUTS:
+        words, lens = synth.reads(ref, 3000, 150, 1000, 0.1, 0.2, 22)
+        check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
+
+
+def test_stats_iteration_bound():
+    # SA_MATCH_STATS: steps per boundary search never exceed ceil(log2(n+2)); joint lo+hi <= 2x
+    ref = synth.reference(synth.REF_REPEAT, 1_000_000, 41)
+    words, lens = synth.reads(ref, 50_000, 20, 100, 0.1, 0.0, 42)
+    idx = sa.Index(ref)
+    st = torch.empty(50_000, dtype=torch.int32, device="cuda")
+    got = gpu_match(idx, words, lens, stats=st)
+    S = oracle.encode(ref)
+    assert np.array_equal(got, oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32))
+    steps = st.cpu().numpy().view(np.uint32) & 0xFFFF
+    import math
+    assert steps.max() <= 2 * math.ceil(math.log2(len(ref) + 2))
 
 
 def test_symbol_error_reports_position():
@@ -175,11 +205,12 @@ def test_lowercase_reference():
 
 # ---- BASELINE.json configs ----------------------------------------------------------------------
 
-def test_c1_full_parity():
+@pytest.mark.parametrize("plain", LAYOUTS)
+def test_c1_full_parity(plain):
     c = synth.CONFIGS["C1"]
     ref = c.reference()
     words, lens = c.reads(ref)
-    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens)
+    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
     assert idx.k == 9
     # the 10k exact reads all hit
     assert (got[:, 1] > got[:, 0]).sum() >= 10_000 * 0.99
@@ -189,24 +220,27 @@ def test_c1_full_parity():
     assert np.array_equal(idx.match_host(words, lens, chunk=3000), got)
 
 
-def test_c2_full_parity():
+@pytest.mark.parametrize("plain", LAYOUTS)
+def test_c2_full_parity(plain):
     c = synth.CONFIGS["C2"]
     ref = c.reference()
     words, lens = c.reads(ref)
-    check_full(ref.tobytes(), words=words, lens=lens)
+    check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
 
 
-def test_repeat_rich_parity_small():
+@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("k", [0, 14])
+def test_repeat_rich_parity_small(plain, k):
     ref = synth.reference(synth.REF_REPEAT, 3_000_000, 33)
     words, lens = synth.reads(ref, 200_000, 16, 160, 0.1, 0.01, 34)
-    check_full(ref.tobytes(), words=words, lens=lens)
+    check_full(ref.tobytes(), words=words, lens=lens, plain=plain, k=k)
 
 
-def test_locate_parity():
-    c = synth.CONFIGS["C2"]
+@pytest.mark.parametrize("plain", LAYOUTS)
+def test_locate_parity(plain):
     ref = synth.reference(synth.REF_REPEAT, 500_000, 5)
     words, lens = synth.reads(ref, 20_000, 8, 40, 0.1, 0.0, 6)
-    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens)
+    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
     offs, pos = idx.locate(torch.from_numpy(got.view(np.int32)).cuda())
     offs = offs.cpu().numpy()
     pos = pos.cpu().numpy().view(np.uint32)
