@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--layout", default="records", choices=["records", "plain"],
                     help="SA layout: 16-byte records caching 48 bases (default) or plain uint32 SA")
     ap.add_argument("--simple", action="store_true", help="one read per thread (no lane refill), for A/B")
+    ap.add_argument("--presort", action="store_true", help="order reads by their first 16 bases (timed)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -272,16 +273,26 @@ def main():
     log(f"{Q} reads/rank generated + uploaded in {time.time() - t0:.1f}s")
 
     stream = torch.cuda.current_stream()
+    flags = sa.SA_MATCH_SIMPLE if args.simple else 0
+    ws = torch.empty(max(1, idx.workspace_size(Q, stride, flags | sa.SA_MATCH_STATS)), dtype=torch.uint8, device=dev)
+    perm = torch.empty(Q, dtype=torch.int32, device=dev) if args.presort else None
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(args.steps)]
 
-    def step():
-        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, simple=args.simple)
+    def step(i=None):
+        # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
+        if args.presort:
+            idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws)
+        if i is not None:
+            ev[i][0].record(stream)
+        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, simple=args.simple, workspace=ws, order=perm)
+        if i is not None:
+            ev[i][1].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
     # ---- timed region ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -291,9 +302,7 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for i in range(args.steps):
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
+            step(i)
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -322,15 +331,17 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
-            "roofline": roofline, "clocks": sampler.result(), "gpu_launches": args.steps,
+            "roofline": roofline, "clocks": sampler.result(),
+            "gpu_launches": args.steps * (2 if args.presort else 1),
+            "library_launches_per_step": "CUB onesweep radix sort (4 passes of 8 bits)" if args.presort else 0,
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
-            "shards": summary_all, "layout": args.layout, "kernel_mode": "simple" if args.simple else "lane-refill",
+            "shards": summary_all, "layout": args.layout, "kernel_mode": ("simple" if args.simple else "lane-refill") + ("+presort" if args.presort else ""),
             "index_bytes": idx.device_bytes}
 
     # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
-    st = torch.empty(Q, dtype=torch.int32, device=dev)
     chk = torch.empty_like(out)
-    idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, stats=st)
+    _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, simple=args.simple,
+                      workspace=ws, order=perm)
     torch.cuda.synchronize()
     if not torch.equal(chk, out):
         raise RuntimeError("instrumented launch disagrees with the timed launches")

@@ -79,6 +79,10 @@ typedef struct {
                               uint32 per query = steps | (text windows fetched << 16); the
                               workspace must then hold >= 4*Q bytes */
 #define SA_MATCH_SIMPLE 2u /* one query per thread, no lane refill (for A/B measurement) */
+#define SA_MATCH_PRESORT 4u /* order the batch by the reads' first 16 bases (CUB radix sort in the
+                               workspace) before the search, so that neighbouring threads walk the
+                               same region of the suffix array; results still land at the reads'
+                               original positions.  Requires Q < 2^32. */
 
 /* Build the index of ref_ascii[0..n) (host memory, case-insensitive ACGT) on
  * the device: validate + pack to 2 bits/base, build the suffix array on the
@@ -109,17 +113,30 @@ sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
 /* Match Q packed queries (the hot path).
  *   q_words   dev, Q*stride_words uint64, layout above.
  *   q_len     dev, Q uint32 lengths, or NULL: every query has fixed_len bases.
+ *   order     dev, Q uint32 permutation (from sa_match_order) or NULL: the order in which thread
+ *             slots take reads.  It never changes a result, only which reads run side by side.
  *   out_lohi  dev, 2Q uint32: out_lohi[2q] = lo, out_lohi[2q+1] = hi
  *             (Alg. 1 lines 44-45, res[thd<<1] = LB, res[(thd<<1)+1] = RB, reading A8).
- *   workspace dev scratch of sa_match_workspace_size() bytes (may be NULL if that is 0;
- *             >= 4*Q bytes with SA_MATCH_STATS).
- *   flags     0, or SA_MATCH_STATS / SA_MATCH_SIMPLE (above).
+ *   workspace dev scratch of sa_match_workspace_size(..., flags, ...) bytes (may be NULL if
+ *             that is 0).  With SA_MATCH_STATS its first 4*Q bytes receive the statistics.
+ *   flags     0, or any of SA_MATCH_STATS / SA_MATCH_SIMPLE / SA_MATCH_PRESORT (above).
  * Requirements: every length m <= 32*stride_words (longer lengths are clamped) and
  * m <= 65535.  Q == 0 is a no-op.  Errors: SA_EINVAL.  Asynchronous on `stream`. */
-sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, size_t *bytes);
+sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, uint32_t flags,
+                                  size_t *bytes);
 sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
-                         uint32_t stride_words, uint64_t Q, uint32_t *out_lohi, void *workspace, size_t ws_bytes,
-                         uint32_t flags, void *stream);
+                         uint32_t stride_words, uint64_t Q, const uint32_t *order, uint32_t *out_lohi,
+                         void *workspace, size_t ws_bytes, uint32_t flags, void *stream);
+
+/* The read ordering of SA_MATCH_PRESORT as its own step: order (dev, Q uint32) receives a
+ * permutation of [0, Q) that sorts the reads by their first 16 bases (stable).  Passing it as
+ * sa_match_batch's `order` makes thread slot t search read order[t]; results are still written at
+ * each read's own index.  The SURVEY.md Sec. 8(a) a5 row ("query ordering"), the B200 reading of the
+ * paper's "coalesced binary search".  Requires Q < 2^32. */
+sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes);
+sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                         uint32_t stride_words, uint64_t Q, uint32_t *order, void *workspace, size_t ws_bytes,
+                         void *stream);
 
 /* The same match with HOST buffers (page-locked recommended): the queries are
  * streamed host->device in chunks of chunk_Q queries (0 = auto), matched, and

@@ -23,6 +23,7 @@ SA_OK, SA_EINVAL, SA_ESYMBOL, SA_ETOOLONG, SA_ENOMEM, SA_ECUDA, SA_EEMPTY = 0, -
 SA_INDEX_PLAIN = 1          # sa_index_opts.flags: plain uint32 SA instead of 16-byte records
 SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windows << 16 into the workspace
 SA_MATCH_SIMPLE = 2         # sa_match_batch flags: one query per thread (no lane refill)
+SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 16 bases before the search
 _NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
           -6: "SA_EEMPTY"}
 
@@ -43,8 +44,10 @@ _SIGS = {
     "sa_index_export_sa": ([_p, _p], ctypes.c_int),
     "sa_index_export_table": ([_p, _p], ctypes.c_int),
     "sa_index_export_text": ([_p, _p], ctypes.c_int),
-    "sa_match_workspace_size": ([_p, _u64, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
-    "sa_match_batch": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _sz, _u32, _p], ctypes.c_int),
+    "sa_match_workspace_size": ([_p, _u64, _u32, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
+    "sa_match_batch": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p, _sz, _u32, _p], ctypes.c_int),
+    "sa_match_order_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
+    "sa_match_order": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _sz, _p], ctypes.c_int),
     "sa_match_batch_host": ([_p, _p, _p, _u32, _u32, _u64, _p, _u64], ctypes.c_int),
     "sa_locate_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_locate_offsets": ([_p, _p, _u64, _p, _p, _sz, _p], ctypes.c_int),
@@ -155,15 +158,36 @@ class Index:
         return out
 
     # ---- the hot path ----
-    def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, stats=None,
-              simple: bool = False):
+    def workspace_size(self, Q: int, stride: int, flags: int) -> int:
+        ws = _sz()
+        _check(lib().sa_match_workspace_size(self._h, Q, stride, flags, ctypes.byref(ws)), "sa_match_workspace_size")
+        return ws.value
+
+    def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None):
+        """sa_match_order: a permutation of the reads sorted by their first 16 bases (CUDA int32 [Q])."""
+        import torch
+        Q, stride = words.shape
+        need = _sz()
+        _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(need)), "sa_match_order_workspace_size")
+        if workspace is None or workspace.numel() < need.value:
+            workspace = torch.empty(max(1, need.value), dtype=torch.uint8, device=words.device)
+        if out is None:
+            out = torch.empty(Q, dtype=torch.int32, device=words.device)
+        _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(out),
+                                    _dptr(workspace), need.value, _stream_ptr(stream)), "sa_match_order")
+        return out
+
+    def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
+              simple: bool = False, presort: bool = False, workspace=None, order=None):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
         lens:  CUDA int32 tensor [Q] (uint32 lengths) or None with fixed_len.
-        stats: optional CUDA int32 tensor [Q] -> per-query steps | text windows << 16 (SA_MATCH_STATS).
-        simple: one query per thread (SA_MATCH_SIMPLE, for A/B measurement).
-        Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi); view it as uint32 on the host.
+        simple / presort: SA_MATCH_SIMPLE / SA_MATCH_PRESORT (include/sa.h).
+        order: optional CUDA int32 [Q] permutation from order() (thread slot t takes read order[t]).
+        workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
+        Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
+        and, with want_stats, also an int32 tensor [Q] of steps | text windows << 16 (SA_MATCH_STATS).
         """
         import torch
         assert words.is_cuda and words.dtype == torch.int64 and words.dim() == 2 and words.is_contiguous()
@@ -175,12 +199,16 @@ class Index:
         if out is None:
             out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
-        flags = (SA_MATCH_SIMPLE if simple else 0) | (SA_MATCH_STATS if stats is not None else 0)
-        if stats is not None:
-            assert stats.is_cuda and stats.numel() >= Q and stats.element_size() == 4
-        _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(out),
-                                    _dptr(stats), 0 if stats is None else 4 * Q, flags, _stream_ptr(stream)),
+        flags = (SA_MATCH_SIMPLE if simple else 0) | (SA_MATCH_STATS if want_stats else 0) | \
+                (SA_MATCH_PRESORT if presort else 0)
+        need = self.workspace_size(Q, stride, flags) if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
+        if need and (workspace is None or workspace.numel() < need):
+            workspace = torch.empty(need, dtype=torch.uint8, device=words.device)
+        _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
+                                    _dptr(out), _dptr(workspace) if need else None, need, flags, _stream_ptr(stream)),
                "sa_match_batch")
+        if want_stats:
+            return out, workspace[: 4 * Q].view(torch.int32)
         return out
 
     def match_host(self, words: np.ndarray, lens: Optional[np.ndarray] = None, fixed_len: Optional[int] = None,

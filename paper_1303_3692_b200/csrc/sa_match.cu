@@ -36,6 +36,7 @@ struct MatchArgs {
     uint64_t Q;
     uint32_t *__restrict__ out;
     uint32_t *__restrict__ stats;      // SA_MATCH_STATS
+    const uint32_t *__restrict__ perm; // SA_MATCH_PRESORT: thread slot t handles read perm[t]
 };
 
 // Query words: QW > 0 -> registers (fully unrolled so indices are static); QW == 0 -> global.
@@ -169,7 +170,8 @@ enum : int { M_IDLE = 0, M_JOINT, M_HI, M_SHORT_LO, M_SHORT_HI };
 template <int QW, bool REC, bool STATS>
 __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // slot; read q = perm[t] or t
+    uint64_t q = 0;
     const uint32_t k = a.k;
     QueryWords<QW> P;
     uint64_t pk01 = 0;
@@ -181,9 +183,10 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     bool split = false, first = true;
     for (;;) {
         if (mode == M_IDLE) {
-            if (!first) q += nthreads;
+            if (!first) t += nthreads;
             first = false;
-            if (q >= a.Q) break;
+            if (t >= a.Q) break;
+            q = a.perm ? (uint64_t)__ldg(a.perm + t) : t;
             // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
             m = min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
             P.load(a.words + q * a.stride, (m + 31) >> 5);
@@ -300,6 +303,62 @@ cudaError_t launch_match_qw(const MatchArgs &a, bool rec, bool stats, bool simpl
     return stats ? launch_match_t<QW, false, true>(a, simple, st) : launch_match_t<QW, false, false>(a, simple, st);
 }
 
+// ---- presort (SA_MATCH_PRESORT) ---------------------------------------------------------------
+// key = the read's first 16 bases (masked to its length), value = read index
+__global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens,
+                               uint32_t fixed_len, uint32_t stride, uint64_t Q, uint32_t *__restrict__ keys,
+                               uint32_t *__restrict__ perm) {
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = min(lens ? __ldg(lens + q) : fixed_len, 32u * stride);
+        const uint64_t w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
+        keys[q] = (uint32_t)((w0 & prefix_mask(min(m, 16u))) >> 32);
+        perm[q] = (uint32_t)q;
+    }
+}
+
+struct PresortLayout {
+    size_t stats = 0, keys_in = 0, keys_out = 0, perm_in = 0, perm_out = 0, cub = 0, cub_bytes = 0, total = 0;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// workspace of sa_match_order (order_only: the permutation goes to the caller's buffer) and of
+// sa_match_batch (stats first, then, with SA_MATCH_PRESORT, the same sort scratch + the permutation)
+sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, PresortLayout &L) {
+    size_t off = 0;
+    if (stats) { L.stats = off; off = align256(off + Q * 4); }
+    if (presort) {
+        if (Q >= (1ull << 32)) { sa_set_error("read ordering needs Q < 2^32"); return SA_EINVAL; }
+        L.keys_in = off; off = align256(off + Q * 4);
+        L.keys_out = off; off = align256(off + Q * 4);
+        L.perm_in = off; off = align256(off + Q * 4);
+        if (!order_only) { L.perm_out = off; off = align256(off + Q * 4); }
+        size_t b = 0;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                                        (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)Q, 0, 32);
+        if (e != cudaSuccess) { sa_set_error("order size query: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+        L.cub = off;
+        L.cub_bytes = b;
+        off = align256(off + b);
+    }
+    L.total = off;
+    return SA_OK;
+}
+
+sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len, uint32_t stride, uint64_t Q,
+                      uint8_t *ws, const PresortLayout &L, uint32_t *order, cudaStream_t st) {
+    uint32_t *keys_in = reinterpret_cast<uint32_t *>(ws + L.keys_in);
+    uint32_t *keys_out = reinterpret_cast<uint32_t *>(ws + L.keys_out);
+    uint32_t *perm_in = reinterpret_cast<uint32_t *>(ws + L.perm_in);
+    uint64_t blocks = (Q + 255) / 256;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, Q, keys_in, perm_in);
+    SA_CUDA_TRY(cudaGetLastError());
+    size_t b = L.cub_bytes;
+    SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0, 32, st));
+    return SA_OK;
+}
+
 // ---- locate -----------------------------------------------------------------------------------
 struct CountOp {
     const uint32_t *lohi;
@@ -340,19 +399,49 @@ sa_status check_match_args(const sa_index *idx, const uint64_t *q_words, const u
 }  // namespace
 
 // ---- C ABI ------------------------------------------------------------------------------------
-extern "C" sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, size_t *bytes) {
+extern "C" sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, uint32_t flags,
+                                             size_t *bytes) {
     sa_clear_error();
     if (!idx || !bytes) { sa_set_error("NULL argument"); return SA_EINVAL; }
-    (void)Q;
     (void)stride_words;
-    *bytes = 0;  // the match itself needs no scratch; SA_MATCH_STATS needs 4*Q bytes
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    PresortLayout L;
+    SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, flags & SA_MATCH_PRESORT, false, L));
+    *bytes = L.total;
     return SA_OK;
 }
 
+extern "C" sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes) {
+    sa_clear_error();
+    if (!bytes) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    PresortLayout L;
+    SA_TRY(presort_layout(Q, false, true, true, L));
+    *bytes = L.total;
+    return SA_OK;
+}
+
+extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
+                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t *order,
+                                    void *workspace, size_t ws_bytes, void *stream) {
+    sa_clear_error();
+    SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, order));
+    if (Q == 0) return SA_OK;
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    PresortLayout L;
+    SA_TRY(presort_layout(Q, false, true, true, L));
+    if (!workspace || ws_bytes < L.total) {
+        sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+        return SA_EINVAL;
+    }
+    return order_reads(q_words, q_len, fixed_len, stride_words, Q, static_cast<uint8_t *>(workspace), L, order,
+                       (cudaStream_t)stream);
+}
+
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
-                              uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, bool simple,
-                              cudaStream_t st) {
+                              uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *perm,
+                              bool simple, cudaStream_t st) {
     MatchArgs a;
+    a.perm = perm;
     a.text = idx->text;
     a.sa = idx->sa;
     a.rec = idx->rec;
@@ -377,23 +466,34 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
 }
 
 extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
-                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t *out_lohi,
-                                    void *workspace, size_t ws_bytes, uint32_t flags, void *stream) {
+                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, const uint32_t *order,
+                                    uint32_t *out_lohi, void *workspace, size_t ws_bytes, uint32_t flags,
+                                    void *stream) {
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
-    if (flags & ~(SA_MATCH_STATS | SA_MATCH_SIMPLE)) { sa_set_error("unknown flags 0x%x", flags); return SA_EINVAL; }
-    uint32_t *stats = nullptr;
-    if (flags & SA_MATCH_STATS) {
-        if (!workspace || ws_bytes < Q * sizeof(uint32_t)) {
-            sa_set_error("SA_MATCH_STATS needs a workspace of >= 4*Q bytes");
-            return SA_EINVAL;
-        }
-        stats = static_cast<uint32_t *>(workspace);
+    if (flags & ~(SA_MATCH_STATS | SA_MATCH_SIMPLE | SA_MATCH_PRESORT)) {
+        sa_set_error("unknown flags 0x%x", flags);
+        return SA_EINVAL;
     }
     if (Q == 0) return SA_OK;
     SA_CUDA_TRY(cudaSetDevice(idx->device));
-    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats,
-                        (flags & SA_MATCH_SIMPLE) != 0, (cudaStream_t)stream);
+    const bool presort = (flags & SA_MATCH_PRESORT) && !order;
+    PresortLayout L;
+    SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, presort, false, L));
+    if (L.total > 0 && (!workspace || ws_bytes < L.total)) {
+        sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+        return SA_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *ws = static_cast<uint8_t *>(workspace);
+    uint32_t *stats = (flags & SA_MATCH_STATS) ? reinterpret_cast<uint32_t *>(ws + L.stats) : nullptr;
+    if (presort) {
+        uint32_t *perm = reinterpret_cast<uint32_t *>(ws + L.perm_out);
+        SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, ws, L, perm, st));
+        order = perm;
+    }
+    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order,
+                        (flags & SA_MATCH_SIMPLE) != 0, st);
 }
 
 extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
@@ -438,7 +538,7 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, false, st));
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr, false, st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }

@@ -25,12 +25,14 @@ def _text(s):
     return s.encode("ascii") if isinstance(s, str) else s
 
 
-def gpu_match(idx, words, lens=None, fixed_len=None, simple=False, stats=None):
+def gpu_match(idx, words, lens=None, fixed_len=None, simple=False, presort=False, want_stats=False):
     w = torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).cuda()
     l = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).cuda()
-    out = idx.match(w, l, fixed_len=fixed_len, simple=simple, stats=stats)
+    res = idx.match(w, l, fixed_len=fixed_len, simple=simple, presort=presort, want_stats=want_stats)
     torch.cuda.synchronize()
-    return out.cpu().numpy().view(np.uint32)
+    if want_stats:
+        return res[0].cpu().numpy().view(np.uint32), res[1].cpu().numpy().view(np.uint32)
+    return res.cpu().numpy().view(np.uint32)
 
 
 LAYOUTS = [False, True]  # records (default), plain SA
@@ -48,11 +50,11 @@ def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=Tr
     if queries is not None:
         words, lens = synth.pack_strings(queries)
     want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
-    for simple in (False, True):
-        got = gpu_match(idx, words, lens, simple=simple)
+    for simple, presort in ((False, False), (True, False), (True, True), (False, True)):
+        got = gpu_match(idx, words, lens, simple=simple, presort=presort)
         bad = np.nonzero((got != want).any(axis=1))[0]
-        assert bad.size == 0, f"{bad.size} mismatches (simple={simple}), first q={bad[0]}: got {got[bad[0]]} " \
-                              f"want {want[bad[0]]}"
+        assert bad.size == 0, f"{bad.size} mismatches (simple={simple}, presort={presort}), first q={bad[0]}: " \
+                              f"got {got[bad[0]]} want {want[bad[0]]}"
     return idx, S, sa_ref, got
 
 
@@ -183,13 +185,33 @@ def test_stats_iteration_bound():
     ref = synth.reference(synth.REF_REPEAT, 1_000_000, 41)
     words, lens = synth.reads(ref, 50_000, 20, 100, 0.1, 0.0, 42)
     idx = sa.Index(ref)
-    st = torch.empty(50_000, dtype=torch.int32, device="cuda")
-    got = gpu_match(idx, words, lens, stats=st)
+    got, st = gpu_match(idx, words, lens, want_stats=True)
     S = oracle.encode(ref)
     assert np.array_equal(got, oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32))
-    steps = st.cpu().numpy().view(np.uint32) & 0xFFFF
+    steps = st & 0xFFFF
     import math
     assert steps.max() <= 2 * math.ceil(math.log2(len(ref) + 2))
+
+
+def test_order_is_a_sorted_permutation_and_keeps_results():
+    ref = synth.reference(synth.REF_REPEAT, 2_000_000, 51)
+    words, lens = synth.reads(ref, 100_000, 10, 100, 0.1, 0.0, 52)
+    idx = sa.Index(ref, k=14)
+    w = torch.from_numpy(words.view(np.int64)).cuda()
+    l = torch.from_numpy(lens.view(np.int32)).cuda()
+    order = idx.order(w, l).cpu().numpy().view(np.uint32)
+    assert np.array_equal(np.sort(order), np.arange(100_000, dtype=np.uint32))
+    key = ((words[:, 0] >> np.uint64(32)).astype(np.uint64))
+    m = lens.astype(np.int64)
+    short = m < 16
+    key[short] &= ((np.uint64(0xFFFFFFFF) << (np.uint64(2) * (np.uint64(16) - m[short].astype(np.uint64)))) &
+                   np.uint64(0xFFFFFFFF))
+    ks = key[order]
+    assert np.all(ks[1:] >= ks[:-1])
+    base = idx.match(w, l)
+    for simple in (False, True):
+        got = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda(), simple=simple)
+        assert torch.equal(got, base)
 
 
 def test_symbol_error_reports_position():
