@@ -1,20 +1,25 @@
-"""Random-access gather roofline sweep on the local GPU (measurement tool; prints one JSON per point)."""
+"""Random-access gather roofline sweep on the local GPU (measurement tool; prints one JSON per point).
+
+Footprint sweep at 32-B accesses: separates the DRAM random-sector rate from address-translation
+(TLB reach) effects; access-size sweep at 16 GiB; dependent-chain latency."""
 import json
-import sys
 import os
+import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1303_3692_b200 as sa  # noqa: E402
 
-for nbytes in (16 << 30,):
-    for acc in (4, 8, 16, 32):
-        for mult in (1, 2, 4, 8):
-            r = sa.random_gather(0, buffer_bytes=nbytes, access_bytes=acc, n_threads=148 * 2048 * mult, loads=64)
-            r.update(buffer=nbytes, threads=148 * 2048 * mult)
-            print(json.dumps(r), flush=True)
-r = sa.random_gather(0, buffer_bytes=16 << 30, access_bytes=32, n_threads=148 * 2048 * 2, loads=64, dependent=True)
-r.update(dependent=True)
-print(json.dumps(r))
-r = sa.random_gather(0, buffer_bytes=64 << 20, access_bytes=32, n_threads=148 * 2048 * 4, loads=64)
-r.update(buffer=64 << 20, note="L2-resident")
-print(json.dumps(r))
+T = 148 * 2048 * 4
+for nbytes in (64 << 20, 256 << 20, 1 << 30, 4 << 30, 16 << 30, 64 << 30):
+    r = sa.random_gather(0, buffer_bytes=nbytes, access_bytes=32, n_threads=T, loads=64)
+    r.update(buffer=nbytes, threads=T, sweep="footprint")
+    print(json.dumps(r), flush=True)
+for acc in (4, 8, 16, 32):
+    r = sa.random_gather(0, buffer_bytes=16 << 30, access_bytes=acc, n_threads=T, loads=64)
+    r.update(buffer=16 << 30, threads=T, sweep="access_bytes")
+    print(json.dumps(r), flush=True)
+for nbytes in (256 << 20, 16 << 30):
+    r = sa.random_gather(0, buffer_bytes=nbytes, access_bytes=32, n_threads=148 * 2048, loads=64, dependent=True)
+    r.update(buffer=nbytes, dependent=True, sweep="latency")
+    r["ns_per_dependent_load"] = r["ms"] * 1e6 / 64
+    print(json.dumps(r), flush=True)
