@@ -48,11 +48,11 @@ def parse():
     ap.add_argument("--config", default="C4", choices=sorted(synth.CONFIGS))
     ap.add_argument("--m", type=int, default=None, help="C5 read length (16..1000)")
     ap.add_argument("--q", type=int, default=None, help="override reads per GPU")
-    ap.add_argument("--k", type=int, default=0, help="k-mer bracket k (0 = auto)")
-    ap.add_argument("--layout", default="records", choices=["records", "plain"],
-                    help="SA layout: 16-byte records caching 48 bases (default) or plain uint32 SA")
-    ap.add_argument("--simple", action="store_true", help="one read per thread (no lane refill), for A/B")
-    ap.add_argument("--presort", action="store_true", help="order reads by their first 16 bases (timed)")
+    ap.add_argument("--k", type=int, default=0, help="k-mer bracket k (0 = auto: floor(log4 n)+1, <= 16)")
+    ap.add_argument("--layout", default="rec16", choices=["rec16", "rec32", "plain"],
+                    help="SA layout: 16-byte records caching 48 bases (default), 32-byte records caching 112 "
+                         "bases, or a plain uint32 SA")
+    ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -254,7 +254,7 @@ def main():
     ref = cfg.reference()
     log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
     t0 = time.time()
-    idx = sa.Index(ref, k=args.k, device=local, plain=(args.layout == "plain"))
+    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout)
     torch.cuda.synchronize()
     log(f"index built in {time.time() - t0:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
     t0 = time.time()
@@ -273,18 +273,19 @@ def main():
     log(f"{Q} reads/rank generated + uploaded in {time.time() - t0:.1f}s")
 
     stream = torch.cuda.current_stream()
-    flags = sa.SA_MATCH_SIMPLE if args.simple else 0
-    ws = torch.empty(max(1, idx.workspace_size(Q, stride, flags | sa.SA_MATCH_STATS)), dtype=torch.uint8, device=dev)
-    perm = torch.empty(Q, dtype=torch.int32, device=dev) if args.presort else None
+    presort = not args.no_order
+    ws = torch.empty(max(1, idx.workspace_size(Q, stride, sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT)),
+                     dtype=torch.uint8, device=dev)
+    perm = torch.empty(Q, dtype=torch.int32, device=dev) if presort else None
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(args.steps)]
 
     def step(i=None):
         # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
-        if args.presort:
+        if presort:
             idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws)
         if i is not None:
             ev[i][0].record(stream)
-        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, simple=args.simple, workspace=ws, order=perm)
+        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm)
         if i is not None:
             ev[i][1].record(stream)
 
@@ -332,16 +333,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
             "roofline": roofline, "clocks": sampler.result(),
-            "gpu_launches": args.steps * (2 if args.presort else 1),
-            "library_launches_per_step": "CUB onesweep radix sort (4 passes of 8 bits)" if args.presort else 0,
+            "gpu_launches": args.steps * (2 if presort else 1),
+            "library_launches_per_step": "CUB onesweep radix sort (4 passes of 8 bits)" if presort else 0,
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
-            "shards": summary_all, "layout": args.layout, "kernel_mode": ("simple" if args.simple else "lane-refill") + ("+presort" if args.presort else ""),
+            "shards": summary_all, "layout": args.layout, "read_order": "sorted by first 16 bases (sa_match_order, timed)" if presort else "as given",
             "index_bytes": idx.device_bytes}
 
     # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
     chk = torch.empty_like(out)
-    _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, simple=args.simple,
-                      workspace=ws, order=perm)
+    _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws, order=perm)
     torch.cuda.synchronize()
     if not torch.equal(chk, out):
         raise RuntimeError("instrumented launch disagrees with the timed launches")

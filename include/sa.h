@@ -63,22 +63,23 @@ typedef enum {
 
 typedef struct {
     int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device */
-    uint32_t kmer_k;   /* k of the k-mer bracket table, 1..16; 0 = auto (min(12, floor(log4 n))) */
-    uint32_t flags;    /* 0 or SA_INDEX_PLAIN */
+    uint32_t kmer_k;   /* k of the k-mer bracket table, 1..16; 0 = auto (min(16, floor(log4 n) + 1)) */
+    uint32_t flags;    /* 0, SA_INDEX_PLAIN or SA_INDEX_REC32 */
     uint32_t reserved; /* must be 0 */
 } sa_index_opts;
 
-/* sa_index_opts.flags.  Default layout: the suffix array is stored as 16-byte records
- * {SA[r], the 48 bases of suffix SA[r] that follow its first k bases} so that one 32-byte
- * sector per search step decides most comparisons (16 B x n of HBM).  SA_INDEX_PLAIN keeps a
- * plain uint32 SA (4 B x n) and reads the packed text at every step. */
+/* sa_index_opts.flags: the layout of the suffix array in HBM.  Default: 16-byte records
+ * {SA[r], the 48 bases of suffix SA[r] that follow its first k bases} -- one 32-byte sector per
+ * search step decides most comparisons (16 B x n).  SA_INDEX_REC32: 32-byte records caching 112
+ * bases (32 B x n; reads up to k+112 bases never touch the text).  SA_INDEX_PLAIN: a plain uint32
+ * SA (4 B x n); every step also reads the packed text. */
 #define SA_INDEX_PLAIN 1u
+#define SA_INDEX_REC32 2u
 
 /* sa_match_batch flags. */
 #define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace:
                               uint32 per query = steps | (text windows fetched << 16); the
                               workspace must then hold >= 4*Q bytes */
-#define SA_MATCH_SIMPLE 2u /* one query per thread, no lane refill (for A/B measurement) */
 #define SA_MATCH_PRESORT 4u /* order the batch by the reads' first 16 bases (CUB radix sort in the
                                workspace) before the search, so that neighbouring threads walk the
                                same region of the suffix array; results still land at the reads'
@@ -119,7 +120,7 @@ sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
  *             (Alg. 1 lines 44-45, res[thd<<1] = LB, res[(thd<<1)+1] = RB, reading A8).
  *   workspace dev scratch of sa_match_workspace_size(..., flags, ...) bytes (may be NULL if
  *             that is 0).  With SA_MATCH_STATS its first 4*Q bytes receive the statistics.
- *   flags     0, or any of SA_MATCH_STATS / SA_MATCH_SIMPLE / SA_MATCH_PRESORT (above).
+ *   flags     0, or SA_MATCH_STATS and/or SA_MATCH_PRESORT (above).
  * Requirements: every length m <= 32*stride_words (longer lengths are clamped) and
  * m <= 65535.  Q == 0 is a no-op.  Errors: SA_EINVAL.  Asynchronous on `stream`. */
 sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, uint32_t flags,

@@ -21,9 +21,10 @@ LIB_PATH = os.path.join(_HERE, "libsa.so")
 
 SA_OK, SA_EINVAL, SA_ESYMBOL, SA_ETOOLONG, SA_ENOMEM, SA_ECUDA, SA_EEMPTY = 0, -1, -2, -3, -4, -5, -6
 SA_INDEX_PLAIN = 1          # sa_index_opts.flags: plain uint32 SA instead of 16-byte records
+SA_INDEX_REC32 = 2          # sa_index_opts.flags: 32-byte records caching 112 bases
 SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windows << 16 into the workspace
-SA_MATCH_SIMPLE = 2         # sa_match_batch flags: one query per thread (no lane refill)
 SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 16 bases before the search
+LAYOUTS = {"rec16": 0, "rec32": SA_INDEX_REC32, "plain": SA_INDEX_PLAIN}
 _NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
           -6: "SA_EEMPTY"}
 
@@ -104,16 +105,17 @@ class Index:
     """Suffix-array index of one reference on one GPU (``sa_index_create``).
 
     ref: str / bytes / numpy uint8 array of ACGT (case-insensitive).  k: bracket-table k (0 = auto).
-    plain: keep a plain uint32 SA (SA_INDEX_PLAIN) instead of the default 16-byte records.
+    layout: "rec16" (default, 16-byte records caching 48 bases), "rec32" (32-byte records, 112 bases)
+    or "plain" (uint32 SA; every step reads the packed text).
     """
 
-    def __init__(self, ref, k: int = 0, device: Optional[int] = None, plain: bool = False):
+    def __init__(self, ref, k: int = 0, device: Optional[int] = None, layout: str = "rec16"):
         if isinstance(ref, str):
             ref = ref.encode("ascii")
         arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
             np.ascontiguousarray(ref, dtype=np.uint8)
-        opts = _Opts(-1 if device is None else int(device), int(k), SA_INDEX_PLAIN if plain else 0, 0)
-        self.plain = bool(plain)
+        opts = _Opts(-1 if device is None else int(device), int(k), LAYOUTS[layout], 0)
+        self.layout = layout
         h = _p()
         _check(lib().sa_index_create(arr.ctypes.data if arr.size else None, arr.size, ctypes.byref(opts),
                                      ctypes.byref(h)), "sa_index_create")
@@ -178,12 +180,12 @@ class Index:
         return out
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
-              simple: bool = False, presort: bool = False, workspace=None, order=None):
+              presort: bool = False, workspace=None, order=None):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
         lens:  CUDA int32 tensor [Q] (uint32 lengths) or None with fixed_len.
-        simple / presort: SA_MATCH_SIMPLE / SA_MATCH_PRESORT (include/sa.h).
+        presort: SA_MATCH_PRESORT (include/sa.h): order the reads inside the call.
         order: optional CUDA int32 [Q] permutation from order() (thread slot t takes read order[t]).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
@@ -199,8 +201,7 @@ class Index:
         if out is None:
             out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
-        flags = (SA_MATCH_SIMPLE if simple else 0) | (SA_MATCH_STATS if want_stats else 0) | \
-                (SA_MATCH_PRESORT if presort else 0)
+        flags = (SA_MATCH_STATS if want_stats else 0) | (SA_MATCH_PRESORT if presort else 0)
         need = self.workspace_size(Q, stride, flags) if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
         if need and (workspace is None or workspace.numel() < need):
             workspace = torch.empty(need, dtype=torch.uint8, device=words.device)

@@ -51,7 +51,8 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     }
     sa_index_opts o{-1, 0, 0, 0};
     if (opts) o = *opts;
-    if ((o.flags & ~SA_INDEX_PLAIN) != 0 || o.reserved != 0) {
+    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32)) != 0 || o.flags == (SA_INDEX_PLAIN | SA_INDEX_REC32) ||
+        o.reserved != 0) {
         sa_set_error("unknown opts.flags bits / reserved must be 0");
         return SA_EINVAL;
     }
@@ -74,11 +75,11 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     if (!idx) { sa_set_error("host allocation failed"); cudaSetDevice(prev); return SA_ENOMEM; }
     idx->device = dev;
     idx->n = n;
-    idx->plain = (o.flags & SA_INDEX_PLAIN) != 0;
+    idx->layout = (o.flags & SA_INDEX_PLAIN) ? 0 : (o.flags & SA_INDEX_REC32) ? 2 : 1;
     uint32_t k = o.kmer_k;
-    if (k == 0) {  // auto: floor(log4 n), at most 12 (a 64 MiB table)
+    if (k == 0) {  // auto: floor(log4 n) + 1 (mean bracket < 1 suffix), at most 16 (a 16 GiB table)
         k = 1;
-        while (k < 12 && (1ull << (2 * (k + 1))) <= n) ++k;
+        while (k < 16 && (1ull << (2 * k)) <= n) ++k;
     }
     idx->k = k;
     cudaStream_t st = nullptr;

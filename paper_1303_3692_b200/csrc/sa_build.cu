@@ -288,35 +288,46 @@ sa_status build_sa(sa_index *idx, cudaStream_t st) {
     return SA_OK;
 }
 
-// SA records: {SA[r], bases k+32..k+47 of the suffix, bases k..k+31 (lo word, hi word)}; bases past n are 0.
+// SA records (layouts in sa_search.cuh); bases past n read as 0 and are masked by length at search time.
+//   L_REC16: {SA[r], bases k+32..k+47 (high half), bases k..k+31 (lo, hi)}
+//   L_REC32: {SA[r], bases k+96..k+111 (high half), bases k..k+31 (lo, hi)}, {k+32..k+63, k+64..k+95}
 __global__ void k_records(const uint64_t *__restrict__ text, uint64_t n, unsigned k, const uint32_t *__restrict__ sa,
-                          uint4 *__restrict__ rec) {
+                          uint4 *__restrict__ rec, int wide) {
     GRID_STRIDE(r, n) {
         const uint64_t s = sa[r];
-        const uint64_t c01 = text_window(text, s + k);
-        const uint64_t c2 = text_window(text, s + k + 32) >> 32;
-        rec[r] = make_uint4((uint32_t)s, (uint32_t)c2, (uint32_t)c01, (uint32_t)(c01 >> 32));
+        const uint64_t c0 = text_window(text, s + k);
+        if (!wide) {
+            const uint64_t c1 = text_window(text, s + k + 32) >> 32;
+            rec[r] = make_uint4((uint32_t)s, (uint32_t)c1, (uint32_t)c0, (uint32_t)(c0 >> 32));
+        } else {
+            const uint64_t c1 = text_window(text, s + k + 32);
+            const uint64_t c2 = text_window(text, s + k + 64);
+            const uint64_t c3 = text_window(text, s + k + 96) >> 32;
+            rec[2 * r] = make_uint4((uint32_t)s, (uint32_t)c3, (uint32_t)c0, (uint32_t)(c0 >> 32));
+            rec[2 * r + 1] = make_uint4((uint32_t)c1, (uint32_t)(c1 >> 32), (uint32_t)c2, (uint32_t)(c2 >> 32));
+        }
     }
 }
 
-__global__ void k_extract_sa(const uint4 *__restrict__ rec, uint64_t count, uint32_t *__restrict__ out) {
-    GRID_STRIDE(r, count) { out[r] = rec[r].x; }
+__global__ void k_extract_sa(const uint4 *__restrict__ rec, uint64_t count, unsigned per, uint32_t *__restrict__ out) {
+    GRID_STRIDE(r, count) { out[r] = rec[r * per].x; }
 }
 
 }  // namespace
 
 sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out) {
     const uint64_t n = idx->n;
-    if (idx->plain) {
+    if (idx->layout == 0) {
         SA_CUDA_TRY(cudaMemcpy(host_out, idx->sa, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
         return SA_OK;
     }
+    const unsigned per = idx->layout == 2 ? 2 : 1;
     const uint64_t CH = 1ull << 28;
     DevBuf<uint32_t> tmp;
     SA_TRY(tmp.alloc(n < CH ? n : CH, nullptr, "SA export staging"));
     for (uint64_t off = 0; off < n; off += CH) {
         const uint64_t c = (n - off < CH) ? n - off : CH;
-        k_extract_sa<<<grid_for(c), kThreads>>>(idx->rec + off, c, tmp.p);
+        k_extract_sa<<<grid_for(c), kThreads>>>(idx->rec + off * per, c, per, tmp.p);
         SA_CUDA_TRY(cudaGetLastError());
         SA_CUDA_TRY(cudaMemcpy(host_out + off, tmp.p, c * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     }
@@ -362,17 +373,18 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
     SA_CUDA_TRY(cudaGetLastError());
     // ---- 4. SA records (default layout) ----
     uint64_t sa_bytes = n * sizeof(uint32_t);
-    if (!idx->plain) {
+    if (idx->layout != 0) {
+        const uint64_t per = idx->layout == 2 ? 2 : 1;
         SA_CUDA_TRY(cudaStreamSynchronize(st));
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-        SA_CUDA_TRY(cudaMalloc(&idx->rec, n * sizeof(uint4)));
-        k_records<<<grid_for(n), kThreads, 0, st>>>(idx->text, n, idx->k, idx->sa, idx->rec);
+        SA_CUDA_TRY(cudaMalloc(&idx->rec, n * per * sizeof(uint4)));
+        k_records<<<grid_for(n), kThreads, 0, st>>>(idx->text, n, idx->k, idx->sa, idx->rec, per == 2);
         SA_CUDA_TRY(cudaGetLastError());
         SA_CUDA_TRY(cudaStreamSynchronize(st));
         SA_CUDA_TRY(cudaFree(idx->sa));
         idx->sa = nullptr;
-        sa_bytes = n * sizeof(uint4);
+        sa_bytes = n * per * sizeof(uint4);
     }
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     idx->device_bytes = idx->n_words * 8 + sa_bytes + (K + 1) * 4;

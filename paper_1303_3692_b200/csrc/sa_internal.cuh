@@ -70,8 +70,7 @@ struct DevBuf {
 
 // ---------------------------------------------------------------------------------------------
 // the index (immutable after create)
-constexpr uint64_t kGuardWords = 4;  // zero words past the text: windows up to base n + 95 are readable
-constexpr uint32_t kCacheBases = 48; // bases cached per SA record (after the first k)
+constexpr uint64_t kGuardWords = 6;  // zero words past the text: windows up to base n + 159 are readable
 
 // SA values of the layout: base pointer + stride in uint32 units
 struct SaView {
@@ -84,9 +83,9 @@ struct sa_index {
     uint32_t k = 0;          // k-mer bracket table
     uint64_t n_words = 0;    // packed text words incl. kGuardWords zero guard words
     uint64_t *text = nullptr;    // dev: 2-bit MSB-first, zero-padded past n (kGuardWords zero words)
-    bool plain = false;          // SA_INDEX_PLAIN: sa[] only; else rec[] only
-    uint32_t *sa = nullptr;      // dev: n entries (plain layout)
-    uint4 *rec = nullptr;        // dev: n records {SA[r], cache bases k+32..k+47, cache bases k..k+31 (lo, hi)}
+    int layout = 1;              // sa_search::L_PLAIN (0), L_REC16 (1), L_REC32 (2)
+    uint32_t *sa = nullptr;      // dev: n entries (L_PLAIN)
+    uint4 *rec = nullptr;        // dev: n records of 1 (L_REC16) or 2 (L_REC32) uint4, see sa_search.cuh
     uint32_t *table = nullptr;   // dev: 4^k + 1 entries
     uint64_t device_bytes = 0;
     uint32_t build_rounds = 0;   // prefix-doubling rounds after the initial sort
@@ -118,7 +117,8 @@ __device__ __forceinline__ uint64_t prefix_mask(unsigned L) {
 }
 
 inline SaView sa_view(const sa_index *idx) {
-    return idx->plain ? SaView{idx->sa, 1u} : SaView{reinterpret_cast<const uint32_t *>(idx->rec), 4u};
+    if (idx->layout == 0) return SaView{idx->sa, 1u};
+    return SaView{reinterpret_cast<const uint32_t *>(idx->rec), idx->layout == 2 ? 8u : 4u};
 }
 
 // build / match entry points implemented in sa_build.cu / sa_match.cu

@@ -1,17 +1,5 @@
-// sa_match.cu -- the hot path: per-query SA interval [lo, hi) by binary search (Sec. IV,
-// Alg. 1 `cudaGeneBinSearch`, L173-230), plus locate and the host-buffer pipeline.
-//
-// B200 design, not a translation of Alg. 1:
-//  * one thread per query (Alg. 1 line 2's mapping) with the query held in registers
-//    (2 bits/base, MSB-first words) instead of the per-block shared tiles of lines 5, 14-15 (which
-//    race as written, reading A9);
-//  * the first k bases index the k-mer bracket table T: the search starts in
-//    (T[x]-1, T[x+1]) instead of Alg. 1's (left, right) = (-1, n) (reading A4);
-//  * Alg. 1's tiled do-while compare (lines 10-17) becomes a 32-bases-per-step compare of two
-//    packed words (xor + clz; unsigned order of MSB-first words is lexicographic order);
-//  * the LB and RB loops (lines 6-23 and 25-42, directions corrected per reading A6) run jointly:
-//    one descent until the first pivot equal to P, then the RB search continues from that split;
-//  * Manber-Myers skipping: compares start at min(lcp(P, t_L), lcp(P, t_R)).
+// sa_match.cu -- host side of the hot path: launch of the search kernel (sa_search.cuh), read
+// ordering (sa_match_order), the host-buffer pipeline, locate, and their C ABI entry points.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -20,287 +8,28 @@
 
 #include "sa_internal.cuh"
 
+#include "sa_search.cuh"
+
 namespace {
 
-struct MatchArgs {
-    const uint64_t *__restrict__ text;
-    const uint32_t *__restrict__ sa;   // plain layout
-    const uint4 *__restrict__ rec;     // record layout
-    const uint32_t *__restrict__ table;
-    uint64_t n;
-    uint32_t k;
-    const uint64_t *__restrict__ words;
-    const uint32_t *__restrict__ lens;
-    uint32_t fixed_len;
-    uint32_t stride;
-    uint64_t Q;
-    uint32_t *__restrict__ out;
-    uint32_t *__restrict__ stats;      // SA_MATCH_STATS
-    const uint32_t *__restrict__ perm; // SA_MATCH_PRESORT: thread slot t handles read perm[t]
-};
+using sa_search::MatchArgs;
 
-// Query words: QW > 0 -> registers (fully unrolled so indices are static); QW == 0 -> global.
-template <int QW>
-struct QueryWords {
-    uint64_t w[QW];
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw) {
-#pragma unroll
-        for (int j = 0; j < QW; ++j) w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
-    }
-    __device__ __forceinline__ uint64_t first() const { return w[0]; }
-    __device__ __forceinline__ uint64_t word(int j) const { return j < QW ? w[j] : 0ull; }
-};
-template <>
-struct QueryWords<0> {
-    const uint64_t *p;
-    uint32_t nw;
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n) { p = q; nw = n; }
-    __device__ __forceinline__ uint64_t first() const { return __ldg(reinterpret_cast<const unsigned long long *>(p)); }
-    __device__ __forceinline__ uint64_t word(int j) const {
-        return (uint32_t)j < nw ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
-    }
-};
-
-// One 32-base step of the compare: word j of P against the text at s + 32j.
-// Returns 1 when decided (sign/lcp set), 0 to continue.
-__device__ __forceinline__ int cmp_word(const uint64_t *__restrict__ text, uint64_t s, uint64_t slen, uint32_t m,
-                                        uint32_t j, uint64_t pw, int &sign, uint32_t &lcp) {
-    const uint32_t base = j << 5;
-    const uint32_t plen = min(32u, m - base);
-    const uint64_t rem = slen > base ? slen - base : 0;
-    const uint32_t L = rem < plen ? (uint32_t)rem : plen;
-    if (L) {
-        const uint64_t tw = text_window(text, s + base);
-        const uint64_t mask = prefix_mask(L);
-        const uint64_t a = pw & mask, b = tw & mask;
-        if (a != b) {
-            lcp = base + ((uint32_t)__clzll((long long)(a ^ b)) >> 1);
-            sign = a > b ? 1 : -1;
-            return 1;
-        }
-    }
-    if (L < plen) {  // the suffix ended first: it is a proper prefix of P (reading A7)
-        lcp = base + L;
-        sign = 1;
-        return 1;
-    }
-    return 0;
-}
-
-// sign(P - t_s), t_s = S[s .. min(s+m, n)), comparing from word skip/32 on; lcp = lcp(P, t_s).
-template <int QW>
-__device__ __forceinline__ void compare(const uint64_t *__restrict__ text, uint64_t n, uint64_t s,
-                                        const QueryWords<QW> &P, uint32_t m, uint32_t skip, int &sign,
-                                        uint32_t &lcp) {
-    const uint64_t slen = n - s;
-    const uint32_t nw = (m + 31) >> 5;
-    const uint32_t j0 = skip >> 5;
-    if constexpr (QW > 0) {
-#pragma unroll
-        for (int j = 0; j < QW; ++j) {
-            if ((uint32_t)j >= j0 && (uint32_t)j < nw) {
-                if (cmp_word(text, s, slen, m, (uint32_t)j, P.w[j], sign, lcp)) return;
-            }
-        }
-    } else {
-        for (uint32_t j = j0; j < nw; ++j) {
-            const uint64_t pw = __ldg(reinterpret_cast<const unsigned long long *>(P.p) + j);
-            if (cmp_word(text, s, slen, m, j, pw, sign, lcp)) return;
-        }
-    }
-    sign = 0;
-    lcp = m;
-}
-
-// Compare P (m >= k, inside its k-mer bracket) with the suffix of SA record r.  The record caches
-// the 48 bases after the first k, which every long suffix in the bracket shares with P; the text
-// is read only when those 48 bases are equal and more remain, or for the < k suffixes shorter
-// than k (which can sit at the end of a bracket without sharing its k-mer).
-template <int QW>
-__device__ __forceinline__ void rec_compare(const uint64_t *__restrict__ text, uint64_t n, uint32_t k, const uint4 r,
-                                            const QueryWords<QW> &P, uint64_t pk01, uint32_t pk2, uint32_t m,
-                                            uint32_t skip, int &sign, uint32_t &lcp, uint32_t &texts) {
-    const uint64_t s = r.x;
-    const uint64_t len = n - s;
-    if (len < k || skip >= k + kCacheBases) {
-        ++texts;
-        compare<QW>(text, n, s, P, m, len < k ? 0u : skip, sign, lcp);
-        return;
-    }
-    const uint32_t avail = (uint32_t)((m < len ? (uint64_t)m : len) - k);  // bases after k present in both
-    const uint64_t c01 = ((uint64_t)r.w << 32) | r.z;
-    const uint64_t mask1 = prefix_mask(min(32u, avail));
-    const uint64_t a1 = pk01 & mask1, b1 = c01 & mask1;
-    if (a1 != b1) {
-        lcp = k + ((uint32_t)__clzll((long long)(a1 ^ b1)) >> 1);
-        sign = a1 > b1 ? 1 : -1;
-        return;
-    }
-    if (avail > 32) {
-        const uint32_t L2 = min(16u, avail - 32);
-        const uint32_t mask2 = L2 >= 16 ? ~0u : ~(~0u >> (2 * L2));
-        const uint32_t a2 = pk2 & mask2, b2 = r.y & mask2;
-        if (a2 != b2) {
-            lcp = k + 32 + ((uint32_t)__clz((int)(a2 ^ b2)) >> 1);
-            sign = a2 > b2 ? 1 : -1;
-            return;
-        }
-        if (avail > kCacheBases) {
-            ++texts;
-            compare<QW>(text, n, s, P, m, k + kCacheBases, sign, lcp);
-            return;
-        }
-    }
-    // every base present in both is equal
-    if (m <= len) { sign = 0; lcp = m; }            // P is a prefix of the suffix (case 1)
-    else { sign = 1; lcp = (uint32_t)len; }          // the suffix is a proper prefix of P (reading A7)
-}
-
-enum : int { M_IDLE = 0, M_JOINT, M_HI, M_SHORT_LO, M_SHORT_HI };
-
-// The search as a per-lane state machine.  Each loop iteration performs ONE binary-search step
-// for whatever query the lane currently holds; a lane whose query is finished writes {lo, hi} and
-// immediately takes its next query (grid-stride), so lanes of a warp stay busy even though reads
-// need very different numbers of steps (repeats: up to ~32, unique reads: ~9).
-//   M_JOINT     LB rule (R moves when P <= t) over the k-mer bracket, remembering the first pivot
-//               where P is a prefix of the suffix (the split);
-//   M_HI        RB rule (R moves when P < t) over (split, R at the split);
-//   M_SHORT_*   m < k: LB then RB rule over the two small windows below T[xa] and T[xb].
-// L is kept as L+1 (Lp1) so every bound fits uint32.
-template <int QW, bool REC, bool STATS>
-__global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
-    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // slot; read q = perm[t] or t
-    uint64_t q = 0;
-    const uint32_t k = a.k;
-    QueryWords<QW> P;
-    uint64_t pk01 = 0;
-    uint32_t pk2 = 0, m = 0;
-    uint32_t Lp1 = 0, R = 0, lcpL = 0, lcpR = 0;
-    uint32_t sLp1 = 0, sR = 0, slcpR = 0, lo = 0;
-    uint32_t nsteps = 0, ntexts = 0;
-    int mode = M_IDLE;
-    bool split = false, first = true;
-    for (;;) {
-        if (mode == M_IDLE) {
-            if (!first) t += nthreads;
-            first = false;
-            if (t >= a.Q) break;
-            q = a.perm ? (uint64_t)__ldg(a.perm + t) : t;
-            // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
-            m = min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
-            P.load(a.words + q * a.stride, (m + 31) >> 5);
-            nsteps = ntexts = 0;
-            lcpL = lcpR = 0;
-            if (m == 0) {  // the empty query is a prefix of every suffix (reading A12)
-                lo = 0;
-                Lp1 = R = (uint32_t)a.n;
-                mode = M_HI;
-            } else if (m >= k) {
-                // all suffixes before T[x] are < P, all from T[x+1] on are > P
-                const uint64_t x = P.first() >> (64 - 2 * k);
-                Lp1 = __ldg(a.table + x);
-                R = __ldg(a.table + x + 1);
-                split = false;
-                mode = M_JOINT;
-                if (REC) {
-                    const uint64_t w0 = P.word(0), w1 = P.word(1), w2 = P.word(2);
-                    pk01 = (w0 << (2 * k)) | (w1 >> (64 - 2 * k));
-                    pk2 = (uint32_t)(((w1 << (2 * k)) | (w2 >> (64 - 2 * k))) >> 32);
-                }
-            } else {
-                // m < k: lo in [T[xa]-(k-m), T[xa]], hi in [T[xb]-(k-1), T[xb]] with xa = x.a^(k-m),
-                // xb = (x+1).a^(k-m); searched over T[.]-k .. T[.]
-                const uint64_t x = P.first() >> (64 - 2 * m);
-                const uint32_t Ta = __ldg(a.table + (x << (2 * (k - m))));
-                const uint32_t Tb = __ldg(a.table + ((x + 1) << (2 * (k - m))));
-                Lp1 = Ta > k ? Ta - k : 0;
-                R = Ta;
-                sLp1 = Tb > k ? Tb - k : 0;
-                sR = Tb;
-                mode = M_SHORT_LO;
-            }
-        }
-        // finished intervals: move to the next phase or emit the result
-        while (mode != M_IDLE && R <= Lp1) {
-            if (mode == M_JOINT) {
-                lo = R;
-                if (split) {
-                    Lp1 = sLp1; R = sR; lcpL = m; lcpR = slcpR;
-                    mode = M_HI;
-                    continue;
-                }
-            } else if (mode == M_SHORT_LO) {
-                lo = R;
-                Lp1 = sLp1; R = sR; lcpL = lcpR = 0;
-                mode = M_SHORT_HI;
-                continue;
-            }
-            // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
-            const uint32_t hi = (mode == M_JOINT) ? lo : R;
-            reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
-            if (STATS) a.stats[q] = nsteps | (ntexts << 16);
-            mode = M_IDLE;
-        }
-        if (mode == M_IDLE) continue;
-        // ---- one binary-search step ----
-        const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
-        int sign;
-        uint32_t lcp;
-        const uint32_t skip = min(lcpL, lcpR);
-        if constexpr (REC) {
-            const uint4 r = __ldg(a.rec + p);
-            if (mode <= M_HI) {
-                rec_compare<QW>(a.text, a.n, k, r, P, pk01, pk2, m, skip, sign, lcp, ntexts);
-            } else {
-                ++ntexts;
-                compare<QW>(a.text, a.n, r.x, P, m, skip, sign, lcp);
-            }
-        } else {
-            const uint64_t s = __ldg(a.sa + p);
-            ++ntexts;
-            compare<QW>(a.text, a.n, s, P, m, skip, sign, lcp);
-        }
-        ++nsteps;
-        if (mode == M_JOINT && sign == 0 && !split) {  // first pivot with P a prefix of its suffix
-            split = true;
-            sLp1 = p + 1;
-            sR = R;
-            slcpR = lcpR;
-        }
-        const bool go_left = sign < 0 || (sign == 0 && (mode == M_JOINT || mode == M_SHORT_LO));
-        if (go_left) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
-    }
-}
-
-template <int QW, bool REC, bool STATS>
-cudaError_t launch_match_t(const MatchArgs &a, bool simple, cudaStream_t st) {
+template <int QW, int L, bool STATS>
+cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     const int threads = 256;
-    uint64_t blocks;
-    if (simple) {
-        blocks = (a.Q + threads - 1) / threads;  // one query per thread
-    } else {
-        static int per_sm[64] = {0};
-        static int sms[64] = {0};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 64 && per_sm[dev] == 0) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], k_match<QW, REC, STATS>, threads, 0);
-            cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-        }
-        const uint64_t resident = (uint64_t)(dev < 64 ? per_sm[dev] * sms[dev] : 148 * 4);
-        const uint64_t need = (a.Q + threads - 1) / threads;
-        blocks = need < resident ? need : resident;  // persistent: one wave, lanes refill
-    }
-    if (blocks == 0) blocks = 1;
-    k_match<QW, REC, STATS><<<(unsigned)blocks, threads, 0, st>>>(a);
+    const uint64_t blocks = (a.Q + threads - 1) / threads;
+    sa_search::k_match<QW, L, STATS><<<(unsigned)blocks, threads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
 template <int QW>
-cudaError_t launch_match_qw(const MatchArgs &a, bool rec, bool stats, bool simple, cudaStream_t st) {
-    if (rec) return stats ? launch_match_t<QW, true, true>(a, simple, st) : launch_match_t<QW, true, false>(a, simple, st);
-    return stats ? launch_match_t<QW, false, true>(a, simple, st) : launch_match_t<QW, false, false>(a, simple, st);
+cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t st) {
+    using namespace sa_search;
+    switch (layout) {
+    case L_PLAIN: return stats ? launch_t<QW, L_PLAIN, true>(a, st) : launch_t<QW, L_PLAIN, false>(a, st);
+    case L_REC32: return stats ? launch_t<QW, L_REC32, true>(a, st) : launch_t<QW, L_REC32, false>(a, st);
+    default: return stats ? launch_t<QW, L_REC16, true>(a, st) : launch_t<QW, L_REC16, false>(a, st);
+    }
 }
 
 // ---- presort (SA_MATCH_PRESORT) ---------------------------------------------------------------
@@ -438,10 +167,9 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
 }
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
-                              uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *perm,
-                              bool simple, cudaStream_t st) {
+                              uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *order,
+                              cudaStream_t st) {
     MatchArgs a;
-    a.perm = perm;
     a.text = idx->text;
     a.sa = idx->sa;
     a.rec = idx->rec;
@@ -455,12 +183,13 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.Q = Q;
     a.out = out;
     a.stats = stats;
-    const bool rec = !idx->plain, st_on = stats != nullptr;
+    a.order = order;
+    const bool st_on = stats != nullptr;
     cudaError_t e;
-    if (stride <= 1) e = launch_match_qw<1>(a, rec, st_on, simple, st);
-    else if (stride <= 2) e = launch_match_qw<2>(a, rec, st_on, simple, st);
-    else if (stride <= 4) e = launch_match_qw<4>(a, rec, st_on, simple, st);
-    else e = launch_match_qw<0>(a, rec, st_on, simple, st);
+    if (stride <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
+    else if (stride <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
+    else if (stride <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
+    else e = launch_qw<0>(a, idx->layout, st_on, st);
     if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
     return SA_OK;
 }
@@ -471,7 +200,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
                                     void *stream) {
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
-    if (flags & ~(SA_MATCH_STATS | SA_MATCH_SIMPLE | SA_MATCH_PRESORT)) {
+    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT)) {
         sa_set_error("unknown flags 0x%x", flags);
         return SA_EINVAL;
     }
@@ -492,8 +221,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, ws, L, perm, st));
         order = perm;
     }
-    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order,
-                        (flags & SA_MATCH_SIMPLE) != 0, st);
+    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, st);
 }
 
 extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
@@ -538,7 +266,7 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr, false, st));
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr, st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }

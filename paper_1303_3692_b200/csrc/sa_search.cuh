@@ -1,0 +1,295 @@
+// sa_search.cuh -- device side of the hot path: per-read SA interval [lo, hi) by binary search
+// (Sec. IV, Alg. 1 `cudaGeneBinSearch`, L173-230), re-designed for B200:
+//
+//  * one thread per read (Alg. 1 line 2's mapping), the read held in registers at 2 bits per
+//    base (MSB-first words) instead of the per-block shared tiles of lines 5, 14-15 (which race as
+//    written, reading A9);
+//  * the first k bases index the k-mer bracket table T: the search starts in (T[x]-1, T[x+1])
+//    instead of Alg. 1's undefined (left, right) (reading A4: (-1, n));
+//  * Alg. 1's tiled do-while compare (lines 10-17) becomes a 32-bases-per-step compare of two packed
+//    words (xor + clz; the unsigned order of MSB-first words is lexicographic order);
+//  * the SA is stored as records {SA[r], bases k .. k+C-1 of that suffix} (C = 48 or 112), so one
+//    32-byte sector per step decides the compare; the packed text is read only past the cache;
+//  * the LB and RB loops (lines 6-23 and 25-42, directions corrected per reading A6) run jointly:
+//    one descent until the first pivot equal to P (the split), then the RB search continues from it;
+//  * Manber-Myers skipping: text compares start at min(lcp(P, t_L), lcp(P, t_R)).
+#pragma once
+
+#include "sa_internal.cuh"
+
+namespace sa_search {
+
+// SA layouts (sa_index::layout)
+enum : int { L_PLAIN = 0, L_REC16 = 1, L_REC32 = 2 };
+
+struct MatchArgs {
+    const uint64_t *__restrict__ text;
+    const uint32_t *__restrict__ sa;    // L_PLAIN
+    const uint4 *__restrict__ rec;      // L_REC16 (1 uint4 per suffix) / L_REC32 (2 uint4 per suffix)
+    const uint32_t *__restrict__ table;
+    uint64_t n;
+    uint32_t k;
+    const uint64_t *__restrict__ words;
+    const uint32_t *__restrict__ lens;
+    uint32_t fixed_len;
+    uint32_t stride;
+    uint64_t Q;
+    uint32_t *__restrict__ out;
+    uint32_t *__restrict__ stats;       // SA_MATCH_STATS
+    const uint32_t *__restrict__ order; // thread slot t takes read order[t] (or t)
+};
+
+// ---- the read ---------------------------------------------------------------------------------
+// QW > 0: QW words in registers (loops over them are fully unrolled so indices are static);
+// QW == 0: long reads, words read from global memory (L1-cached) as needed.
+template <int QW>
+struct QueryWords {
+    uint64_t w[QW];
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw) {
+#pragma unroll
+        for (int j = 0; j < QW; ++j)
+            w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+    }
+    __device__ __forceinline__ uint64_t first() const { return w[0]; }
+    __device__ __forceinline__ uint64_t word(int j) const { return j < QW ? w[j] : 0ull; }
+};
+template <>
+struct QueryWords<0> {
+    const uint64_t *p;
+    uint32_t nw;
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n) { p = q; nw = n; }
+    __device__ __forceinline__ uint64_t first() const { return __ldg(reinterpret_cast<const unsigned long long *>(p)); }
+    __device__ __forceinline__ uint64_t word(int j) const {
+        return (uint32_t)j < nw ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+    }
+};
+
+// ---- compare against the packed text --------------------------------------------------------
+// One 32-base step: word j of P against the text at s + 32j.  Returns true when decided.
+__device__ __forceinline__ bool cmp_text_word(const uint64_t *__restrict__ text, uint64_t s, uint64_t slen, uint32_t m,
+                                              uint32_t j, uint64_t pw, int &sign, uint32_t &lcp) {
+    const uint32_t base = j << 5;
+    const uint32_t plen = min(32u, m - base);
+    const uint64_t rem = slen > base ? slen - base : 0;
+    const uint32_t L = rem < plen ? (uint32_t)rem : plen;
+    if (L) {
+        const uint64_t tw = text_window(text, s + base);
+        const uint64_t mask = prefix_mask(L);
+        const uint64_t a = pw & mask, b = tw & mask;
+        if (a != b) {
+            lcp = base + ((uint32_t)__clzll((long long)(a ^ b)) >> 1);
+            sign = a > b ? 1 : -1;
+            return true;
+        }
+    }
+    if (L < plen) {  // the suffix ended first: it is a proper prefix of P (reading A7)
+        lcp = base + L;
+        sign = 1;
+        return true;
+    }
+    return false;
+}
+
+// sign(P - t_s), t_s = S[s .. min(s+m, n)), comparing from word skip/32 on; lcp = lcp(P, t_s).
+template <int QW>
+__device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, uint64_t n, uint64_t s,
+                                             const QueryWords<QW> &P, uint32_t m, uint32_t skip, int &sign,
+                                             uint32_t &lcp) {
+    const uint64_t slen = n - s;
+    const uint32_t nw = (m + 31) >> 5;
+    const uint32_t j0 = skip >> 5;
+    if constexpr (QW > 0) {
+#pragma unroll
+        for (int j = 0; j < QW; ++j) {
+            if ((uint32_t)j >= j0 && (uint32_t)j < nw) {
+                if (cmp_text_word(text, s, slen, m, (uint32_t)j, P.w[j], sign, lcp)) return;
+            }
+        }
+    } else {
+        for (uint32_t j = j0; j < nw; ++j) {
+            if (cmp_text_word(text, s, slen, m, j, P.word((int)j), sign, lcp)) return;
+        }
+    }
+    sign = 0;
+    lcp = m;
+}
+
+// ---- SA records ---------------------------------------------------------------------------------
+// L_REC16: uint4 {SA, bases k+32..k+47 (high half), bases k..k+31 (lo, hi)}               -> 48 bases
+// L_REC32: uint4 {SA, bases k+96..k+111 (high half), bases k..k+31 (lo, hi)},
+//          uint4 {bases k+32..k+63 (lo, hi), bases k+64..k+95 (lo, hi)}                   -> 112 bases
+template <int L>
+struct Rec {
+    static constexpr int kWords = (L == L_REC32) ? 4 : 2;             // 64-bit cache words
+    static constexpr uint32_t kBases = (L == L_REC32) ? 112u : 48u;   // cached bases
+    uint32_t sa;
+    uint64_t c[kWords];  // c[j] = bases k+32j .. k+32j+31 (the last word holds 16)
+    __device__ __forceinline__ void load(const uint4 *__restrict__ rec, uint64_t p) {
+        if constexpr (L == L_REC32) {
+            // one 256-bit load (LDG.E.ENL2.256 on sm_100a): the whole 32-byte record, one sector
+            uint64_t w0, w1, w2, w3;
+            asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
+                : "l"(rec + 2 * p));
+            sa = (uint32_t)w0;
+            c[0] = w1;
+            c[1] = w2;
+            c[2] = w3;
+            c[3] = w0 & 0xFFFFFFFF00000000ull;
+        } else {
+            const uint4 a = __ldg(rec + p);
+            sa = a.x;
+            c[0] = ((uint64_t)a.w << 32) | a.z;
+            c[1] = (uint64_t)a.y << 32;
+        }
+    }
+};
+
+// Bases k+32j .. k+32j+31 of P (k < 32).
+template <int QW>
+__device__ __forceinline__ uint64_t read_after_k(const QueryWords<QW> &P, uint32_t k, int j) {
+    return (P.word(j) << (2 * k)) | (P.word(j + 1) >> (64 - 2 * k));
+}
+
+// Compare P (m >= k, inside its k-mer bracket) with the suffix of a record.  Every suffix with >= k
+// bases in the bracket starts with P's k-mer, so the compare starts at base k on the cached bases;
+// the text is read only when all cached bases are equal and more remain, or for the < k suffixes
+// shorter than k (which can sit at the end of a bracket without sharing its k-mer).
+template <int QW, int L>
+__device__ __forceinline__ void compare_rec(const MatchArgs &a, const Rec<L> &r, const QueryWords<QW> &P, uint32_t m,
+                                            uint32_t skip, int &sign, uint32_t &lcp, uint32_t &texts) {
+    const uint32_t k = a.k;
+    const uint64_t s = r.sa, len = a.n - s;
+    constexpr uint32_t CB = Rec<L>::kBases;
+    if (len < k || skip >= k + CB) {
+        ++texts;
+        compare_text<QW>(a.text, a.n, s, P, m, len < k ? 0u : skip, sign, lcp);
+        return;
+    }
+    const uint32_t avail = (uint32_t)((m < len ? (uint64_t)m : len) - k);  // bases after k present in both
+#pragma unroll
+    for (int j = 0; j < Rec<L>::kWords; ++j) {
+        const uint32_t base = 32u * j;
+        if (base < avail) {
+            const uint32_t Lj = min(min(32u, avail - base), CB - base);
+            const uint64_t mask = prefix_mask(Lj);
+            const uint64_t x = read_after_k<QW>(P, k, j) & mask, y = r.c[j] & mask;
+            if (x != y) {
+                lcp = k + base + ((uint32_t)__clzll((long long)(x ^ y)) >> 1);
+                sign = x > y ? 1 : -1;
+                return;
+            }
+        }
+    }
+    if (avail > CB) {
+        ++texts;
+        compare_text<QW>(a.text, a.n, s, P, m, k + CB, sign, lcp);
+        return;
+    }
+    // every base present in both is equal
+    if (m <= len) { sign = 0; lcp = m; }            // P is a prefix of the suffix (case 1)
+    else { sign = 1; lcp = (uint32_t)len; }          // the suffix is a proper prefix of P (reading A7)
+}
+
+// Probe pivot p: sign(P - t_SA[p]) and lcp.  in_bracket: P has >= k bases and (L, R) lies inside
+// its k-mer bracket, so a record's cache applies.
+template <int QW, int L>
+__device__ __forceinline__ void probe(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint64_t p,
+                                      uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts) {
+    if constexpr (L == L_PLAIN) {
+        const uint64_t s = __ldg(a.sa + p);
+        ++texts;
+        compare_text<QW>(a.text, a.n, s, P, m, skip, sign, lcp);
+    } else {
+        Rec<L> r;
+        r.load(a.rec, p);
+        if (in_bracket) {
+            compare_rec<QW, L>(a, r, P, m, skip, sign, lcp, texts);
+        } else {
+            ++texts;
+            compare_text<QW>(a.text, a.n, r.sa, P, m, skip, sign, lcp);
+        }
+    }
+}
+
+// Binary search over (Lp1-1, R): LB rule (lower: R moves when P <= t) or RB rule (R moves when P < t).
+template <int QW, int L>
+__device__ __forceinline__ uint32_t bound(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint32_t Lp1,
+                                          uint32_t R, uint32_t lcpL, uint32_t lcpR, bool lower, bool in_bracket,
+                                          uint32_t &steps, uint32_t &texts) {
+    while (R > Lp1) {
+        const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
+        int sign;
+        uint32_t lcp;
+        probe<QW, L>(a, P, m, p, min(lcpL, lcpR), in_bracket, sign, lcp, texts);
+        ++steps;
+        if (sign < 0 || (lower && sign == 0)) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+    }
+    return R;
+}
+
+// One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.
+template <int QW, int L>
+__device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint32_t &lo,
+                                            uint32_t &hi, uint32_t &steps, uint32_t &texts) {
+    const uint32_t k = a.k;
+    if (m == 0) {  // the empty read is a prefix of every suffix (reading A12)
+        lo = 0;
+        hi = (uint32_t)a.n;
+        return;
+    }
+    if (m < k) {
+        // lo in [T[xa]-(k-m), T[xa]], hi in [T[xb]-(k-1), T[xb]], xa = x.a^(k-m), xb = (x+1).a^(k-m)
+        // (DESIGN.md "Bracket, short reads"); each searched over (T[.]-k-1, T[.])
+        const uint64_t x = P.first() >> (64 - 2 * m);
+        const uint32_t Ta = __ldg(a.table + (x << (2 * (k - m))));
+        const uint32_t Tb = __ldg(a.table + ((x + 1) << (2 * (k - m))));
+        lo = bound<QW, L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts);
+        hi = bound<QW, L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts);
+        return;
+    }
+    // all suffixes before T[x] are < P, all from T[x+1] on are > P
+    const uint64_t x = P.first() >> (64 - 2 * k);
+    uint32_t Lp1 = __ldg(a.table + x);
+    uint32_t R = __ldg(a.table + x + 1);
+    uint32_t lcpL = 0, lcpR = 0;
+    uint32_t sLp1 = 0, sR = 0, slcpR = 0;
+    bool split = false;
+    while (R > Lp1) {  // LB rule, remembering the first pivot where P is a prefix of the suffix
+        const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
+        int sign;
+        uint32_t lcp;
+        probe<QW, L>(a, P, m, p, min(lcpL, lcpR), true, sign, lcp, texts);
+        ++steps;
+        if (sign == 0 && !split) { split = true; sLp1 = p + 1; sR = R; slcpR = lcpR; }
+        if (sign <= 0) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+    }
+    lo = R;
+    hi = split ? bound<QW, L>(a, P, m, sLp1, sR, m, slcpR, false, true, steps, texts) : lo;
+}
+
+__device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
+    // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
+    return min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
+}
+
+// One read per thread slot, all lanes of a warp in lock step (with sa_match_order the lanes hold
+// lexicographically adjacent reads and walk neighbouring parts of the SA and table).  A persistent,
+// lane-refilling variant (a finished lane takes the next read) was measured slower on B200 at C4
+// (profiles/r01b, r01c: it de-correlates the lanes' addresses and scatters loads and stores).
+template <int QW, int L, bool STATS>
+__global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.Q) return;
+    const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
+    const uint32_t m = read_len(a, q);
+    QueryWords<QW> P;
+    P.load(a.words + q * a.stride, (m + 31) >> 5);
+    uint32_t lo, hi, steps = 0, texts = 0;
+    search_read<QW, L>(a, P, m, lo, hi, steps, texts);
+    // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
+    reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+    if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+}
+
+}  // namespace sa_search

@@ -25,23 +25,23 @@ def _text(s):
     return s.encode("ascii") if isinstance(s, str) else s
 
 
-def gpu_match(idx, words, lens=None, fixed_len=None, simple=False, presort=False, want_stats=False):
+def gpu_match(idx, words, lens=None, fixed_len=None, presort=False, want_stats=False):
     w = torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).cuda()
     l = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).cuda()
-    res = idx.match(w, l, fixed_len=fixed_len, simple=simple, presort=presort, want_stats=want_stats)
+    res = idx.match(w, l, fixed_len=fixed_len, presort=presort, want_stats=want_stats)
     torch.cuda.synchronize()
     if want_stats:
         return res[0].cpu().numpy().view(np.uint32), res[1].cpu().numpy().view(np.uint32)
     return res.cpu().numpy().view(np.uint32)
 
 
-LAYOUTS = [False, True]  # records (default), plain SA
+LAYOUTS = ["rec16", "rec32", "plain"]
 
 
-def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, plain=False):
+def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, layout="rec16"):
     """Build on the GPU; compare SA, table and every interval with the oracle."""
     S = oracle.encode(text_ascii)
-    idx = sa.Index(text_ascii, k=k, plain=plain)
+    idx = sa.Index(text_ascii, k=k, layout=layout)
     sa_ref = oracle.sa_naive(S)
     if check_sa:
         assert np.array_equal(idx.export_sa(), sa_ref)
@@ -50,10 +50,10 @@ def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=Tr
     if queries is not None:
         words, lens = synth.pack_strings(queries)
     want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
-    for simple, presort in ((False, False), (True, False), (True, True), (False, True)):
-        got = gpu_match(idx, words, lens, simple=simple, presort=presort)
+    for presort in (False, True):
+        got = gpu_match(idx, words, lens, presort=presort)
         bad = np.nonzero((got != want).any(axis=1))[0]
-        assert bad.size == 0, f"{bad.size} mismatches (simple={simple}, presort={presort}), first q={bad[0]}: " \
+        assert bad.size == 0, f"{bad.size} mismatches (layout={layout}, presort={presort}), first q={bad[0]}: " \
                               f"got {got[bad[0]]} want {want[bad[0]]}"
     return idx, S, sa_ref, got
 
@@ -101,13 +101,13 @@ def test_paper_example_table1_and_sec4():
 
 # ---- small adversarial texts: SA, table and intervals bit-exact --------------------------------
 
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 @pytest.mark.parametrize("n", [1, 2, 5, 31, 32, 33, 63, 64, 65, 1000, 4097])
 @pytest.mark.parametrize("k", [0, 1, 3, 6, 16])
 def test_random_texts_all_k(n, k, plain):
     rng = random.Random(n * 10 + k)
     text = "".join(rng.choice("ACGT") for _ in range(n))
-    check_full(text, hazard_queries(text, k or 6, rng), k=k, plain=plain)
+    check_full(text, hazard_queries(text, k or 6, rng), k=k, layout=plain)
 
 
 @pytest.mark.parametrize("text", [
@@ -117,10 +117,10 @@ def test_random_texts_all_k(n, k, plain):
     "T" * 777 + "A" * 333,
     "ACGTTGCA" * 900,
 ])
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 def test_periodic_and_homopolymer_texts(text, plain):
     rng = random.Random(len(text))
-    check_full(text, hazard_queries(text, 8, rng), k=8, plain=plain)
+    check_full(text, hazard_queries(text, 8, rng), k=8, layout=plain)
 
 
 def test_homopolymer_closed_form():
@@ -161,7 +161,7 @@ def test_de_bruijn_every_kmer_once():
     assert np.all(got[:, 1] - got[:, 0] == 1)
 
 
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 def test_short_queries_below_k(plain):
     # m < k exercises the widened brackets
     rng = random.Random(7)
@@ -169,15 +169,15 @@ def test_short_queries_below_k(plain):
         text = "".join(rng.choice("AC") for _ in range(n)) + "".join(rng.choice("ACGT") for _ in range(n))
         qs = ["".join(p) for m in range(1, 5) for p in itertools.product("ACGT", repeat=m)]
         qs += [text[-j:] for j in range(1, 12)]
-        check_full(text, qs, k=10, plain=plain)
+        check_full(text, qs, k=10, layout=plain)
 
 
 def test_long_reads_generic_path():
     # stride > 4 words: the generic (global-memory query) kernel, reads up to 1000 bp with long matches
     ref = synth.reference(synth.REF_REPEAT, 400_000, 21)
-    for plain in LAYOUTS:
+    for plain in LAYOUTS:  # the SA layout
         words, lens = synth.reads(ref, 3000, 150, 1000, 0.1, 0.2, 22)
-        check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
+        check_full(ref.tobytes(), words=words, lens=lens, layout=plain)
 
 
 def test_stats_iteration_bound():
@@ -209,9 +209,8 @@ def test_order_is_a_sorted_permutation_and_keeps_results():
     ks = key[order]
     assert np.all(ks[1:] >= ks[:-1])
     base = idx.match(w, l)
-    for simple in (False, True):
-        got = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda(), simple=simple)
-        assert torch.equal(got, base)
+    got = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda())
+    assert torch.equal(got, base)
 
 
 def test_symbol_error_reports_position():
@@ -227,13 +226,13 @@ def test_lowercase_reference():
 
 # ---- BASELINE.json configs ----------------------------------------------------------------------
 
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 def test_c1_full_parity(plain):
     c = synth.CONFIGS["C1"]
     ref = c.reference()
     words, lens = c.reads(ref)
-    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
-    assert idx.k == 9
+    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens, layout=plain)
+    assert idx.k == 10
     # the 10k exact reads all hit
     assert (got[:, 1] > got[:, 0]).sum() >= 10_000 * 0.99
     # same result through the fixed-length path and the host-buffer pipeline
@@ -242,27 +241,27 @@ def test_c1_full_parity(plain):
     assert np.array_equal(idx.match_host(words, lens, chunk=3000), got)
 
 
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 def test_c2_full_parity(plain):
     c = synth.CONFIGS["C2"]
     ref = c.reference()
     words, lens = c.reads(ref)
-    check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
+    check_full(ref.tobytes(), words=words, lens=lens, layout=plain)
 
 
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 @pytest.mark.parametrize("k", [0, 14])
 def test_repeat_rich_parity_small(plain, k):
     ref = synth.reference(synth.REF_REPEAT, 3_000_000, 33)
     words, lens = synth.reads(ref, 200_000, 16, 160, 0.1, 0.01, 34)
-    check_full(ref.tobytes(), words=words, lens=lens, plain=plain, k=k)
+    check_full(ref.tobytes(), words=words, lens=lens, layout=plain, k=k)
 
 
-@pytest.mark.parametrize("plain", LAYOUTS)
+@pytest.mark.parametrize("plain", LAYOUTS)  # the SA layout
 def test_locate_parity(plain):
     ref = synth.reference(synth.REF_REPEAT, 500_000, 5)
     words, lens = synth.reads(ref, 20_000, 8, 40, 0.1, 0.0, 6)
-    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens, plain=plain)
+    idx, S, sa_ref, got = check_full(ref.tobytes(), words=words, lens=lens, layout=plain)
     offs, pos = idx.locate(torch.from_numpy(got.view(np.int32)).cuda())
     offs = offs.cpu().numpy()
     pos = pos.cpu().numpy().view(np.uint32)
