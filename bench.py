@@ -49,10 +49,11 @@ def parse():
     ap.add_argument("--m", type=int, default=None, help="C5 read length (16..1000)")
     ap.add_argument("--q", type=int, default=None, help="override reads per GPU")
     ap.add_argument("--k", type=int, default=0, help="k-mer bracket k (0 = auto: floor(log4 n)+1, <= 16)")
-    ap.add_argument("--layout", default="rec16", choices=["rec16", "rec32", "plain"],
+    ap.add_argument("--layout", default="rec32", choices=["rec16", "rec32", "plain"],
                     help="SA layout: 16-byte records caching 48 bases (default), 32-byte records caching 112 "
                          "bases, or a plain uint32 SA")
     ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
+    ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -139,19 +140,23 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def algorithmic_bytes_per_query(n, k, m, layout="records"):
-    """sector-granular bytes the k-mer-bracket joint search must move per read.
+def algorithmic_bytes_per_query(n, k, m, layout="rec32"):
+    """the sector-granular bytes the k-mer-bracket joint search must move per read.
 
-    D = log2(mean bracket + 1) + 1 search steps (the joint lo/hi search: one descent plus on average
-    one extra level for the hi continuation).
-      plain   : 1 table sector + D x (SA sector + text sector) + read (m/4 B) + result (8 B)
-      records : 1 table sector + D x (record sector) + 1 text sector (verifying the bases past the
-                48 cached ones) + read + result."""
+    D = log2(mean bracket + 1) + 1 search steps (one descent plus on average one extra level for
+    the hi continuation); every random access moves one 32-B sector.
+      plain : 1 table sector + D x (SA sector + text sector)                      + read + result
+      rec16 : 1 table sector + D x (record sector) + 1 text sector (bases past 48) + read + result
+      rec32 : 1 table sector + D x (record sector) [+ 1 text sector if m > k+112]  + read + result
+    read = one 32-B sector per read gathered through the ordering (ceil(m/4) B for m > 128),
+    result = 8 B."""
     bracket = n / float(4 ** k)
     D = math.log2(bracket + 1.0) + 1.0
+    read = max(32.0, math.ceil(m / 4.0))
     if layout == "plain":
-        return 32.0 + D * 64.0 + math.ceil(m / 4.0) + 8.0
-    return 32.0 + D * 32.0 + 32.0 + math.ceil(m / 4.0) + 8.0
+        return 32.0 + D * 64.0 + read + 8.0
+    text = 32.0 if (layout == "rec16" and m > k + 48) or (layout == "rec32" and m > k + 112) else 0.0
+    return 32.0 + D * 32.0 + text + read + 8.0
 
 
 def traffic_per_launch(workload_name):
@@ -282,7 +287,7 @@ def main():
     def step(i=None):
         # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
         if presort:
-            idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws)
+            idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws, key_bases=args.order_bases)
         if i is not None:
             ev[i][0].record(stream)
         idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm)
@@ -334,9 +339,10 @@ def main():
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
             "roofline": roofline, "clocks": sampler.result(),
             "gpu_launches": args.steps * (2 if presort else 1),
-            "library_launches_per_step": "CUB onesweep radix sort (4 passes of 8 bits)" if presort else 0,
+            "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
+                                          if presort else 0),
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
-            "shards": summary_all, "layout": args.layout, "read_order": "sorted by first 16 bases (sa_match_order, timed)" if presort else "as given",
+            "shards": summary_all, "layout": args.layout, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
             "index_bytes": idx.device_bytes}
 
     # ---- search statistics (untimed instrumented launch): steps and text windows per read ----

@@ -80,7 +80,7 @@ typedef struct {
 #define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace:
                               uint32 per query = steps | (text windows fetched << 16); the
                               workspace must then hold >= 4*Q bytes */
-#define SA_MATCH_PRESORT 4u /* order the batch by the reads' first 16 bases (CUB radix sort in the
+#define SA_MATCH_PRESORT 4u /* order the batch by the reads' first 12 bases (CUB radix sort in the
                                workspace) before the search, so that neighbouring threads walk the
                                same region of the suffix array; results still land at the reads'
                                original positions.  Requires Q < 2^32. */
@@ -130,14 +130,15 @@ sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uin
                          void *workspace, size_t ws_bytes, uint32_t flags, void *stream);
 
 /* The read ordering of SA_MATCH_PRESORT as its own step: order (dev, Q uint32) receives a
- * permutation of [0, Q) that sorts the reads by their first 16 bases (stable).  Passing it as
+ * permutation of [0, Q) that sorts the reads by their first key_bases bases (1..16, 0 = 12;
+ * stable; SA_MATCH_PRESORT uses 12).  Passing it as
  * sa_match_batch's `order` makes thread slot t search read order[t]; results are still written at
  * each read's own index.  The SURVEY.md Sec. 8(a) a5 row ("query ordering"), the B200 reading of the
  * paper's "coalesced binary search".  Requires Q < 2^32. */
 sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes);
 sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
-                         uint32_t stride_words, uint64_t Q, uint32_t *order, void *workspace, size_t ws_bytes,
-                         void *stream);
+                         uint32_t stride_words, uint64_t Q, uint32_t key_bases, uint32_t *order, void *workspace,
+                         size_t ws_bytes, void *stream);
 
 /* The same match with HOST buffers (page-locked recommended): the queries are
  * streamed host->device in chunks of chunk_Q queries (0 = auto), matched, and

@@ -48,7 +48,7 @@ _SIGS = {
     "sa_match_workspace_size": ([_p, _u64, _u32, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_match_batch": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p, _sz, _u32, _p], ctypes.c_int),
     "sa_match_order_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
-    "sa_match_order": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _sz, _p], ctypes.c_int),
+    "sa_match_order": ([_p, _p, _p, _u32, _u32, _u64, _u32, _p, _p, _sz, _p], ctypes.c_int),
     "sa_match_batch_host": ([_p, _p, _p, _u32, _u32, _u64, _p, _u64], ctypes.c_int),
     "sa_locate_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_locate_offsets": ([_p, _p, _u64, _p, _p, _sz, _p], ctypes.c_int),
@@ -165,8 +165,9 @@ class Index:
         _check(lib().sa_match_workspace_size(self._h, Q, stride, flags, ctypes.byref(ws)), "sa_match_workspace_size")
         return ws.value
 
-    def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None):
-        """sa_match_order: a permutation of the reads sorted by their first 16 bases (CUDA int32 [Q])."""
+    def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None,
+              key_bases: int = 0):
+        """sa_match_order: a permutation of the reads sorted by their first key_bases bases (0 = 12)."""
         import torch
         Q, stride = words.shape
         need = _sz()
@@ -175,8 +176,8 @@ class Index:
             workspace = torch.empty(max(1, need.value), dtype=torch.uint8, device=words.device)
         if out is None:
             out = torch.empty(Q, dtype=torch.int32, device=words.device)
-        _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(out),
-                                    _dptr(workspace), need.value, _stream_ptr(stream)), "sa_match_order")
+        _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, int(key_bases),
+                                    _dptr(out), _dptr(workspace), need.value, _stream_ptr(stream)), "sa_match_order")
         return out
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,

@@ -74,8 +74,10 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
     return SA_OK;
 }
 
+constexpr uint32_t kDefaultKeyBases = 12;
+
 sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len, uint32_t stride, uint64_t Q,
-                      uint8_t *ws, const PresortLayout &L, uint32_t *order, cudaStream_t st) {
+                      uint32_t key_bases, uint8_t *ws, const PresortLayout &L, uint32_t *order, cudaStream_t st) {
     uint32_t *keys_in = reinterpret_cast<uint32_t *>(ws + L.keys_in);
     uint32_t *keys_out = reinterpret_cast<uint32_t *>(ws + L.keys_out);
     uint32_t *perm_in = reinterpret_cast<uint32_t *>(ws + L.perm_in);
@@ -84,7 +86,10 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, Q, keys_in, perm_in);
     SA_CUDA_TRY(cudaGetLastError());
     size_t b = L.cub_bytes;
-    SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0, 32, st));
+    // only the top 2*key_bases bits of the 16-base key: ceil(2*key_bases/8) radix passes
+    const int begin_bit = 32 - 2 * (int)key_bases;
+    SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, begin_bit,
+                                                32, st));
     return SA_OK;
 }
 
@@ -150,9 +155,11 @@ extern "C" sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes) {
 }
 
 extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
-                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t *order,
-                                    void *workspace, size_t ws_bytes, void *stream) {
+                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t key_bases,
+                                    uint32_t *order, void *workspace, size_t ws_bytes, void *stream) {
     sa_clear_error();
+    if (key_bases > 16) { sa_set_error("key_bases %u > 16", key_bases); return SA_EINVAL; }
+    if (key_bases == 0) key_bases = kDefaultKeyBases;
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, order));
     if (Q == 0) return SA_OK;
     SA_CUDA_TRY(cudaSetDevice(idx->device));
@@ -162,8 +169,8 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
         sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
         return SA_EINVAL;
     }
-    return order_reads(q_words, q_len, fixed_len, stride_words, Q, static_cast<uint8_t *>(workspace), L, order,
-                       (cudaStream_t)stream);
+    return order_reads(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace), L,
+                       order, (cudaStream_t)stream);
 }
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
@@ -218,7 +225,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
     uint32_t *stats = (flags & SA_MATCH_STATS) ? reinterpret_cast<uint32_t *>(ws + L.stats) : nullptr;
     if (presort) {
         uint32_t *perm = reinterpret_cast<uint32_t *>(ws + L.perm_out);
-        SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, ws, L, perm, st));
+        SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, kDefaultKeyBases, ws, L, perm, st));
         order = perm;
     }
     return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, st);

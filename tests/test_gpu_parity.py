@@ -193,21 +193,25 @@ def test_stats_iteration_bound():
     assert steps.max() <= 2 * math.ceil(math.log2(len(ref) + 2))
 
 
-def test_order_is_a_sorted_permutation_and_keeps_results():
+@pytest.mark.parametrize("key_bases", [0, 8, 16])
+def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     ref = synth.reference(synth.REF_REPEAT, 2_000_000, 51)
     words, lens = synth.reads(ref, 100_000, 10, 100, 0.1, 0.0, 52)
     idx = sa.Index(ref, k=14)
     w = torch.from_numpy(words.view(np.int64)).cuda()
     l = torch.from_numpy(lens.view(np.int32)).cuda()
-    order = idx.order(w, l).cpu().numpy().view(np.uint32)
+    order = idx.order(w, l, key_bases=key_bases).cpu().numpy().view(np.uint32)
     assert np.array_equal(np.sort(order), np.arange(100_000, dtype=np.uint32))
-    key = ((words[:, 0] >> np.uint64(32)).astype(np.uint64))
-    m = lens.astype(np.int64)
-    short = m < 16
-    key[short] &= ((np.uint64(0xFFFFFFFF) << (np.uint64(2) * (np.uint64(16) - m[short].astype(np.uint64)))) &
-                   np.uint64(0xFFFFFFFF))
+    kb = key_bases or 12
+    key = (words[:, 0] >> np.uint64(64 - 2 * kb)).astype(np.uint64)
+    m = lens.astype(np.uint64)
+    short = m < kb
+    key[short] &= ~((np.uint64(1) << (np.uint64(2) * (np.uint64(kb) - m[short]))) - np.uint64(1))
     ks = key[order]
     assert np.all(ks[1:] >= ks[:-1])
+    # stable: equal keys keep the reads' input order
+    eq = ks[1:] == ks[:-1]
+    assert np.all(order[1:][eq] > order[:-1][eq])
     base = idx.match(w, l)
     got = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda())
     assert torch.equal(got, base)
