@@ -5,6 +5,7 @@
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "sa_internal.cuh"
 
@@ -14,11 +15,27 @@ namespace {
 
 using sa_search::MatchArgs;
 
+// Occupancy knob for measurement: SA_MATCH_MINBLOCKS=6|8 selects __launch_bounds__(256, 6|8)
+// instantiations (fewer registers per thread, more threads per SM); default lets ptxas choose.
+inline int min_blocks_knob() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SA_MATCH_MINBLOCKS");
+        v = e ? atoi(e) : 0;
+        if (v != 6 && v != 8) v = 0;
+    }
+    return v;
+}
+
 template <int QW, int L, bool STATS>
 cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     const int threads = 256;
-    const uint64_t blocks = (a.Q + threads - 1) / threads;
-    sa_search::k_match<QW, L, STATS><<<(unsigned)blocks, threads, 0, st>>>(a);
+    const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+    switch (min_blocks_knob()) {
+    case 6: sa_search::k_match<QW, L, STATS, 6><<<blocks, threads, 0, st>>>(a); break;
+    case 8: sa_search::k_match<QW, L, STATS, 8><<<blocks, threads, 0, st>>>(a); break;
+    default: sa_search::k_match<QW, L, STATS, 1><<<blocks, threads, 0, st>>>(a); break;
+    }
     return cudaGetLastError();
 }
 
@@ -191,6 +208,9 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.out = out;
     a.stats = stats;
     a.order = order;
+    // one vector load per read row when the row is exactly QW words and suitably aligned
+    const uintptr_t wp = reinterpret_cast<uintptr_t>(q_words);
+    a.vec_rows = (stride == 4 && (wp & 31) == 0) || (stride == 2 && (wp & 15) == 0);
     const bool st_on = stats != nullptr;
     cudaError_t e;
     if (stride <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);

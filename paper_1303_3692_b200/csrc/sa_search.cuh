@@ -37,6 +37,7 @@ struct MatchArgs {
     uint32_t *__restrict__ out;
     uint32_t *__restrict__ stats;       // SA_MATCH_STATS
     const uint32_t *__restrict__ order; // thread slot t takes read order[t] (or t)
+    bool vec_rows;                      // read rows can be loaded with one vector load (aligned, stride == QW)
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -45,7 +46,24 @@ struct MatchArgs {
 template <int QW>
 struct QueryWords {
     uint64_t w[QW];
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw) {
+    // the whole read row in one vector load (one request, one sector) when the stride equals QW:
+    // 256-bit (LDG.E.ENL2.256) for 4 words, 128-bit for 2; rows are then 32- / 16-byte aligned
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw, bool vec) {
+        if constexpr (QW == 4) {
+            if (vec) {
+                asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                    : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+                    : "l"(p));
+                return;
+            }
+        } else if constexpr (QW == 2) {
+            if (vec) {
+                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(p));
+                w[0] = v.x;
+                w[1] = v.y;
+                return;
+            }
+        }
 #pragma unroll
         for (int j = 0; j < QW; ++j)
             w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
@@ -57,7 +75,7 @@ template <>
 struct QueryWords<0> {
     const uint64_t *p;
     uint32_t nw;
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n) { p = q; nw = n; }
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool) { p = q; nw = n; }
     __device__ __forceinline__ uint64_t first() const { return __ldg(reinterpret_cast<const unsigned long long *>(p)); }
     __device__ __forceinline__ uint64_t word(int j) const {
         return (uint32_t)j < nw ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
@@ -144,6 +162,17 @@ struct Rec {
         }
     }
 };
+
+// T[x] and T[x+1]: one aligned 16-byte load unless x sits in the last slot of its 16-byte group.
+__device__ __forceinline__ void table_pair(const uint32_t *__restrict__ T, uint64_t x, uint32_t &a, uint32_t &b) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(T + (x & ~3ull)));
+    switch (x & 3) {
+    case 0: a = v.x; b = v.y; break;
+    case 1: a = v.y; b = v.z; break;
+    case 2: a = v.z; b = v.w; break;
+    default: a = v.w; b = __ldg(T + x + 1); break;
+    }
+}
 
 // Bases k+32j .. k+32j+31 of P (k < 32).
 template <int QW>
@@ -250,8 +279,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
     }
     // all suffixes before T[x] are < P, all from T[x+1] on are > P
     const uint64_t x = P.first() >> (64 - 2 * k);
-    uint32_t Lp1 = __ldg(a.table + x);
-    uint32_t R = __ldg(a.table + x + 1);
+    uint32_t Lp1, R;
+    table_pair(a.table, x, Lp1, R);
     uint32_t lcpL = 0, lcpR = 0;
     uint32_t sLp1 = 0, sR = 0, slcpR = 0;
     bool split = false;
@@ -277,14 +306,14 @@ __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
 // lexicographically adjacent reads and walk neighbouring parts of the SA and table).  A persistent,
 // lane-refilling variant (a finished lane takes the next read) was measured slower on B200 at C4
 // (profiles/r01b, r01c: it de-correlates the lanes' addresses and scatters loads and stores).
-template <int QW, int L, bool STATS>
-__global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
+template <int QW, int L, bool STATS, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.Q) return;
     const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
     const uint32_t m = read_len(a, q);
     QueryWords<QW> P;
-    P.load(a.words + q * a.stride, (m + 31) >> 5);
+    P.load(a.words + q * a.stride, (m + 31) >> 5, a.vec_rows);
     uint32_t lo, hi, steps = 0, texts = 0;
     search_read<QW, L>(a, P, m, lo, hi, steps, texts);
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
