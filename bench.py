@@ -54,6 +54,8 @@ def parse():
                          "bases, or a plain uint32 SA")
     ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
+    ap.add_argument("--rows-ordered", action="store_true",
+                    help="the ordering step also gathers the read rows into order (SA_MATCH_ROWS_ORDERED)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -282,15 +284,22 @@ def main():
     ws = torch.empty(max(1, idx.workspace_size(Q, stride, sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT)),
                      dtype=torch.uint8, device=dev)
     perm = torch.empty(Q, dtype=torch.int32, device=dev) if presort else None
+    rows_ordered = presort and args.rows_ordered
+    owords = torch.empty_like(words) if rows_ordered else None
+    olens = torch.empty_like(lens) if (rows_ordered and lens is not None) else None
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(args.steps)]
 
     def step(i=None):
         # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
         if presort:
-            idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws, key_bases=args.order_bases)
+            idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws, key_bases=args.order_bases,
+                      ordered_words=owords, ordered_lens=olens)
         if i is not None:
             ev[i][0].record(stream)
-        idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm)
+        if rows_ordered:
+            idx.match(owords, olens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm, rows_ordered=True)
+        else:
+            idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm)
         if i is not None:
             ev[i][1].record(stream)
 
@@ -347,7 +356,12 @@ def main():
 
     # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
     chk = torch.empty_like(out)
-    _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws, order=perm)
+    if rows_ordered:
+        _, st = idx.match(owords, olens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
+                          order=perm, rows_ordered=True)
+    else:
+        _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
+                          order=perm)
     torch.cuda.synchronize()
     if not torch.equal(chk, out):
         raise RuntimeError("instrumented launch disagrees with the timed launches")

@@ -84,6 +84,9 @@ typedef struct {
                                workspace) before the search, so that neighbouring threads walk the
                                same region of the suffix array; results still land at the reads'
                                original positions.  Requires Q < 2^32. */
+#define SA_MATCH_ROWS_ORDERED 8u /* q_words / q_len are already in `order` order (sa_match_order's
+                                    ordered_words / ordered_len): thread slot t reads row t and
+                                    writes its interval to out_lohi at read order[t] */
 
 /* Build the index of ref_ascii[0..n) (host memory, case-insensitive ACGT) on
  * the device: validate + pack to 2 bits/base, build the suffix array on the
@@ -134,11 +137,14 @@ sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uin
  * stable; SA_MATCH_PRESORT uses 12).  Passing it as
  * sa_match_batch's `order` makes thread slot t search read order[t]; results are still written at
  * each read's own index.  The SURVEY.md Sec. 8(a) a5 row ("query ordering"), the B200 reading of the
- * paper's "coalesced binary search".  Requires Q < 2^32. */
+ * paper's "coalesced binary search".  Requires Q < 2^32.
+ * ordered_words (dev, Q*stride_words, nullable) / ordered_len (dev, Q, nullable): if given, also
+ * receive the reads' rows / lengths in that order (row t = read order[t]), for SA_MATCH_ROWS_ORDERED. */
 sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes);
 sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
-                         uint32_t stride_words, uint64_t Q, uint32_t key_bases, uint32_t *order, void *workspace,
-                         size_t ws_bytes, void *stream);
+                         uint32_t stride_words, uint64_t Q, uint32_t key_bases, uint32_t *order,
+                         uint64_t *ordered_words, uint32_t *ordered_len, void *workspace, size_t ws_bytes,
+                         void *stream);
 
 /* The same match with HOST buffers (page-locked recommended): the queries are
  * streamed host->device in chunks of chunk_Q queries (0 = auto), matched, and
@@ -159,7 +165,8 @@ sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_
 
 /* Measurement tool (not on the path): random-access gather rate of the
  * device's memory.  Allocates buffer_bytes, then every thread issues `loads`
- * independent (dependent=0) or pointer-chased (dependent=1) loads of
+ * independent (dependent=0) or pointer-chased (dependent=1) loads -- or, with dependent=2,
+ * independent stores -- of
  * access_bytes (4, 8, 16 or 32) at hashed, access_bytes-aligned offsets.
  * *ms = device time of one launch of n_threads threads (CUDA events). */
 sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,

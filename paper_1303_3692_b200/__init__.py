@@ -23,7 +23,8 @@ SA_OK, SA_EINVAL, SA_ESYMBOL, SA_ETOOLONG, SA_ENOMEM, SA_ECUDA, SA_EEMPTY = 0, -
 SA_INDEX_PLAIN = 1          # sa_index_opts.flags: plain uint32 SA instead of 16-byte records
 SA_INDEX_REC32 = 2          # sa_index_opts.flags: 32-byte records caching 112 bases
 SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windows << 16 into the workspace
-SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 16 bases before the search
+SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 12 bases before the search
+SA_MATCH_ROWS_ORDERED = 8   # sa_match_batch flags: rows already arranged in `order` order
 LAYOUTS = {"rec16": 0, "rec32": SA_INDEX_REC32, "plain": SA_INDEX_PLAIN}
 _NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
           -6: "SA_EEMPTY"}
@@ -48,7 +49,7 @@ _SIGS = {
     "sa_match_workspace_size": ([_p, _u64, _u32, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_match_batch": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p, _sz, _u32, _p], ctypes.c_int),
     "sa_match_order_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
-    "sa_match_order": ([_p, _p, _p, _u32, _u32, _u64, _u32, _p, _p, _sz, _p], ctypes.c_int),
+    "sa_match_order": ([_p, _p, _p, _u32, _u32, _u64, _u32, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
     "sa_match_batch_host": ([_p, _p, _p, _u32, _u32, _u64, _p, _u64], ctypes.c_int),
     "sa_locate_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_locate_offsets": ([_p, _p, _u64, _p, _p, _sz, _p], ctypes.c_int),
@@ -166,8 +167,9 @@ class Index:
         return ws.value
 
     def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None,
-              key_bases: int = 0):
-        """sa_match_order: a permutation of the reads sorted by their first key_bases bases (0 = 12)."""
+              key_bases: int = 0, ordered_words=None, ordered_lens=None):
+        """sa_match_order: a permutation of the reads sorted by their first key_bases bases (0 = 12);
+        optionally also the rows / lengths arranged in that order (for match(..., rows_ordered=True))."""
         import torch
         Q, stride = words.shape
         need = _sz()
@@ -177,17 +179,19 @@ class Index:
         if out is None:
             out = torch.empty(Q, dtype=torch.int32, device=words.device)
         _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, int(key_bases),
-                                    _dptr(out), _dptr(workspace), need.value, _stream_ptr(stream)), "sa_match_order")
+                                    _dptr(out), _dptr(ordered_words), _dptr(ordered_lens), _dptr(workspace),
+                                    need.value, _stream_ptr(stream)), "sa_match_order")
         return out
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
-              presort: bool = False, workspace=None, order=None):
+              presort: bool = False, workspace=None, order=None, rows_ordered: bool = False):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
         lens:  CUDA int32 tensor [Q] (uint32 lengths) or None with fixed_len.
         presort: SA_MATCH_PRESORT (include/sa.h): order the reads inside the call.
         order: optional CUDA int32 [Q] permutation from order() (thread slot t takes read order[t]).
+        rows_ordered: words/lens are order()'s ordered_words/ordered_lens (row t is read order[t]).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [Q] of steps | text windows << 16 (SA_MATCH_STATS).
@@ -202,7 +206,8 @@ class Index:
         if out is None:
             out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
-        flags = (SA_MATCH_STATS if want_stats else 0) | (SA_MATCH_PRESORT if presort else 0)
+        flags = (SA_MATCH_STATS if want_stats else 0) | (SA_MATCH_PRESORT if presort else 0) | \
+                (SA_MATCH_ROWS_ORDERED if rows_ordered else 0)
         need = self.workspace_size(Q, stride, flags) if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
         if need and (workspace is None or workspace.numel() < need):
             workspace = torch.empty(need, dtype=torch.uint8, device=words.device)
@@ -248,8 +253,8 @@ class Index:
 
 
 def random_gather(device: int = 0, buffer_bytes: int = 16 << 30, access_bytes: int = 32, n_threads: int = 148 * 2048 * 4,
-                  loads: int = 64, dependent: bool = False) -> dict:
-    """Random-access gather microbenchmark (the roofline denominator for a random-gather kernel)."""
+                  loads: int = 64, dependent: int = 0) -> dict:
+    """Random-access microbenchmark: dependent=0 independent loads, 1 pointer-chased loads, 2 stores."""
     ms = ctypes.c_float()
     _check(lib().sa_tool_random_gather(device, buffer_bytes, access_bytes, n_threads, loads, int(dependent),
                                        ctypes.byref(ms)), "sa_tool_random_gather")

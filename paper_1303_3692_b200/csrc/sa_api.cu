@@ -1,5 +1,6 @@
 // sa_api.cu -- C ABI plumbing of libsa: errors, index lifetime, exports, measurement tool.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -184,6 +185,27 @@ __global__ void k_gather(const uint8_t *__restrict__ buf, uint64_t slot_mask, ui
     if (acc == 0x5eed) sink[0] = acc;  // keeps the loads alive
 }
 
+// mode 2: random stores of BYTES (partial-sector stores below 32 B exercise the L2 / ECC
+// read-modify-write path of a scattered result write)
+template <int BYTES>
+__global__ void k_scatter(uint8_t *__restrict__ buf, uint64_t slot_mask, uint32_t stores) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t h = hash64(tid * 0x9E3779B97F4A7C15ull + 0x7654321ull);
+    for (uint32_t i = 0; i < stores; ++i) {
+        const uint64_t slot = hash64(h + i) & slot_mask;
+        uint8_t *p = buf + slot * BYTES;
+        if constexpr (BYTES == 32) {
+            *reinterpret_cast<ulonglong4 *>(p) = make_ulonglong4(h, i, tid, slot);
+        } else if constexpr (BYTES == 16) {
+            *reinterpret_cast<uint4 *>(p) = make_uint4((uint32_t)h, i, (uint32_t)tid, (uint32_t)slot);
+        } else if constexpr (BYTES == 8) {
+            *reinterpret_cast<unsigned long long *>(p) = h + i;
+        } else {
+            *reinterpret_cast<unsigned int *>(p) = (uint32_t)(h + i);
+        }
+    }
+}
+
 extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes,
                                            uint64_t n_threads, uint32_t loads, int32_t dependent, float *ms) {
     sa_clear_error();
@@ -206,6 +228,15 @@ extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes
     const unsigned threads = 256;
     const unsigned blocks = (unsigned)((n_threads + threads - 1) / threads);
     auto launch = [&]() {
+        if (dependent == 2) {
+            switch (access_bytes) {
+            case 32: k_scatter<32><<<blocks, threads>>>(buf, slots - 1, loads); break;
+            case 16: k_scatter<16><<<blocks, threads>>>(buf, slots - 1, loads); break;
+            case 8: k_scatter<8><<<blocks, threads>>>(buf, slots - 1, loads); break;
+            default: k_scatter<4><<<blocks, threads>>>(buf, slots - 1, loads); break;
+            }
+            return;
+        }
         switch (access_bytes) {
         case 32: k_gather<32><<<blocks, threads>>>(buf, slots - 1, loads, dependent, sink); break;
         case 16: k_gather<16><<<blocks, threads>>>(buf, slots - 1, loads, dependent, sink); break;

@@ -62,6 +62,23 @@ __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_
     }
 }
 
+// row t of the ordered copy = read order[t] (coalesced writes; the reads are gathered once here)
+__global__ void k_gather_rows(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens, uint32_t stride,
+                              uint64_t Q, const uint32_t *__restrict__ order, uint64_t *__restrict__ out_words,
+                              uint32_t *__restrict__ out_lens) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = __ldg(order + t);
+        if (out_words) {
+            if (stride == 4) {
+                reinterpret_cast<ulonglong4 *>(out_words)[t] = reinterpret_cast<const ulonglong4 *>(words)[q];
+            } else {
+                for (uint32_t j = 0; j < stride; ++j) out_words[t * stride + j] = __ldg(words + q * stride + j);
+            }
+        }
+        if (out_lens && lens) out_lens[t] = __ldg(lens + q);
+    }
+}
+
 struct PresortLayout {
     size_t stats = 0, keys_in = 0, keys_out = 0, perm_in = 0, perm_out = 0, cub = 0, cub_bytes = 0, total = 0;
 };
@@ -173,7 +190,8 @@ extern "C" sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes) {
 
 extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
                                     uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t key_bases,
-                                    uint32_t *order, void *workspace, size_t ws_bytes, void *stream) {
+                                    uint32_t *order, uint64_t *ordered_words, uint32_t *ordered_len,
+                                    void *workspace, size_t ws_bytes, void *stream) {
     sa_clear_error();
     if (key_bases > 16) { sa_set_error("key_bases %u > 16", key_bases); return SA_EINVAL; }
     if (key_bases == 0) key_bases = kDefaultKeyBases;
@@ -186,14 +204,25 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
         sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
         return SA_EINVAL;
     }
-    return order_reads(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace), L,
-                       order, (cudaStream_t)stream);
+    SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace), L,
+                       order, (cudaStream_t)stream));
+    if (ordered_words || ordered_len) {
+        const bool vec = stride_words == 4 && (reinterpret_cast<uintptr_t>(q_words) & 31) == 0 &&
+                         (reinterpret_cast<uintptr_t>(ordered_words) & 31) == 0;
+        uint64_t blocks = (Q + 255) / 256;
+        if (blocks > 148ull * 16) blocks = 148ull * 16;
+        k_gather_rows<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(q_words, q_len, vec ? 4u : stride_words, Q,
+                                                                          order, ordered_words, ordered_len);
+        SA_CUDA_TRY(cudaGetLastError());
+    }
+    return SA_OK;
 }
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                               uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *order,
-                              cudaStream_t st) {
+                              bool rows_ordered, cudaStream_t st) {
     MatchArgs a;
+    a.rows_ordered = rows_ordered;
     a.text = idx->text;
     a.sa = idx->sa;
     a.rec = idx->rec;
@@ -227,7 +256,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
                                     void *stream) {
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
-    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT)) {
+    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED)) {
         sa_set_error("unknown flags 0x%x", flags);
         return SA_EINVAL;
     }
@@ -248,7 +277,12 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, kDefaultKeyBases, ws, L, perm, st));
         order = perm;
     }
-    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, st);
+    const bool rows_ordered = (flags & SA_MATCH_ROWS_ORDERED) != 0;
+    if (rows_ordered && (!order || presort)) {
+        sa_set_error("SA_MATCH_ROWS_ORDERED needs the order the rows were arranged in");
+        return SA_EINVAL;
+    }
+    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st);
 }
 
 extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
@@ -293,7 +327,7 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr, st));
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr, false, st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }

@@ -38,6 +38,7 @@ struct MatchArgs {
     uint32_t *__restrict__ stats;       // SA_MATCH_STATS
     const uint32_t *__restrict__ order; // thread slot t takes read order[t] (or t)
     bool vec_rows;                      // read rows can be loaded with one vector load (aligned, stride == QW)
+    bool rows_ordered;                  // SA_MATCH_ROWS_ORDERED: row t is read order[t]
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -310,10 +311,11 @@ template <int QW, int L, bool STATS, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.Q) return;
-    const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
-    const uint32_t m = read_len(a, q);
+    const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;  // the read; its result goes to out[q]
+    const uint64_t row = a.rows_ordered ? t : q;                      // where its bases are
+    const uint32_t m = read_len(a, row);
     QueryWords<QW> P;
-    P.load(a.words + q * a.stride, (m + 31) >> 5, a.vec_rows);
+    P.load(a.words + row * a.stride, (m + 31) >> 5, a.vec_rows);
     uint32_t lo, hi, steps = 0, texts = 0;
     search_read<QW, L>(a, P, m, lo, hi, steps, texts);
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here

@@ -75,7 +75,7 @@ def test_match_argument_errors():
     L = sa.lib()
     # NULL index
     assert L.sa_match_batch(None, None, None, 0, 1, 0, None, None, None, 0, 0, None) == sa.SA_EINVAL
-    assert L.sa_match_order(None, None, None, 0, 1, 0, 0, None, None, 0, None) == sa.SA_EINVAL
+    assert L.sa_match_order(None, None, None, 0, 1, 0, 0, None, None, None, None, 0, None) == sa.SA_EINVAL
     ws = ctypes.c_size_t()
     assert L.sa_locate_workspace_size(10, ctypes.byref(ws)) in (sa.SA_OK, sa.SA_ECUDA)  # CUB asks the device
     assert L.sa_locate_workspace_size(10, None) == sa.SA_EINVAL

@@ -215,6 +215,12 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     base = idx.match(w, l)
     got = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda())
     assert torch.equal(got, base)
+    # the rows arranged in that order (SA_MATCH_ROWS_ORDERED) give the same intervals at the same places
+    ow, ol = torch.empty_like(w), torch.empty_like(l)
+    perm = idx.order(w, l, key_bases=key_bases, ordered_words=ow, ordered_lens=ol)
+    assert torch.equal(ow, w[perm.long()]) and torch.equal(ol, l[perm.long()])
+    got2 = idx.match(ow, ol, order=perm, rows_ordered=True)
+    assert torch.equal(got2, base)
 
 
 def test_symbol_error_reports_position():

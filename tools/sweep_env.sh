@@ -3,7 +3,7 @@
 tag=$1; cfg=$2; shift 2
 for v in "$@"; do
   envs=${v%%|*}; args=${v#*|}
-  name=$(echo "$envs$args" | tr -d ' -=|' )
+  name=$(echo "$envs$args" | tr -c 'A-Za-z0-9' '_' )
   env $envs timeout 600 python bench.py --config $cfg --steps 10 --warmup 3 --no-e2e --no-cpu $args \
      > gpurun_out/sweep_${tag}_${cfg}_${name:-default}.json 2> gpurun_out/sweep_${tag}_${cfg}_${name:-default}.log
   python - "$v" gpurun_out/sweep_${tag}_${cfg}_${name:-default}.json <<'PY'
