@@ -15,27 +15,11 @@ namespace {
 
 using sa_search::MatchArgs;
 
-// Occupancy knob for measurement: SA_MATCH_MINBLOCKS=6|8 selects __launch_bounds__(256, 6|8)
-// instantiations (fewer registers per thread, more threads per SM); default lets ptxas choose.
-inline int min_blocks_knob() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SA_MATCH_MINBLOCKS");
-        v = e ? atoi(e) : 0;
-        if (v != 6 && v != 8) v = 0;
-    }
-    return v;
-}
-
 template <int QW, int L, bool STATS>
 cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     const int threads = 256;
     const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
-    switch (min_blocks_knob()) {
-    case 6: sa_search::k_match<QW, L, STATS, 6><<<blocks, threads, 0, st>>>(a); break;
-    case 8: sa_search::k_match<QW, L, STATS, 8><<<blocks, threads, 0, st>>>(a); break;
-    default: sa_search::k_match<QW, L, STATS, 1><<<blocks, threads, 0, st>>>(a); break;
-    }
+    sa_search::k_match<QW, L, STATS><<<blocks, threads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -223,6 +207,7 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
                               bool rows_ordered, cudaStream_t st) {
     MatchArgs a;
     a.rows_ordered = rows_ordered;
+
     a.text = idx->text;
     a.sa = idx->sa;
     a.rec = idx->rec;

@@ -307,8 +307,8 @@ __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
 // lexicographically adjacent reads and walk neighbouring parts of the SA and table).  A persistent,
 // lane-refilling variant (a finished lane takes the next read) was measured slower on B200 at C4
 // (profiles/r01b, r01c: it de-correlates the lanes' addresses and scatters loads and stores).
-template <int QW, int L, bool STATS, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_match(const MatchArgs a) {
+template <int QW, int L, bool STATS>
+__global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.Q) return;
     const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;  // the read; its result goes to out[q]
