@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-locate", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -371,6 +372,19 @@ def main():
                             "p99_steps": float(torch.quantile(steps_t[:1 << 20], 0.99)),
                             "max_steps": float(steps_t.max())}
     del st, chk
+
+    # ---- locate (separate call): positions SA[lo..hi) of every read ----
+    if not args.no_locate:
+        torch.cuda.synchronize()
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        offs, pos = idx.locate(out, stream=stream)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        line["locate"] = {"ms": l0.elapsed_time(l1), "positions": int(pos.numel()),
+                          "note": "offsets scan + SA gather, one call after the timed region (includes the "
+                                  "device->host read of the total to size the output)"}
+        del offs, pos
 
     # ---- random-gather microbenchmark (context for the roofline; untimed) ----
     if rank == 0:

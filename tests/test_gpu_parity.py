@@ -281,22 +281,30 @@ def test_locate_parity(plain):
         assert np.array_equal(pos[offs[q]:offs[q + 1]], oracle.locate(sa_ref, int(got[q, 0]), int(got[q, 1])))
 
 
-def _full_size_check(cfg, sample=2000, q_count=None):
+def _full_size_check(cfg, sample=2000, q_count=None, layout="rec32"):
+    """The bench configuration (bench.py defaults: rec32 records, auto k, reads ordered by 12 bases)."""
     ref = cfg.reference()
     S = oracle.encode(ref)
-    idx = sa.Index(ref)
+    idx = sa.Index(ref, layout=layout)
     sa_gpu = idx.export_sa()
     assert oracle.check_sa(S, sa_gpu) == -1, "GPU suffix array fails the oracle's SA check"
     words, lens = cfg.reads(ref, q_count=q_count)
-    got = gpu_match(idx, words, None, fixed_len=cfg.m_max) if cfg.m_min == cfg.m_max else gpu_match(idx, words, lens)
+    w = torch.from_numpy(words.view(np.int64)).cuda()
+    l = None if cfg.m_min == cfg.m_max else torch.from_numpy(lens.view(np.int32)).cuda()
+    fixed = cfg.m_max if l is None else None
+    perm = idx.order(w, l, fixed_len=fixed, key_bases=12)
+    got = idx.match(w, l, fixed_len=fixed, order=perm)
+    torch.cuda.synchronize()
+    got = got.cpu().numpy().view(np.uint32)
+    del w, l, perm
     # sampled outputs straight from the definition (no SA)
     rng = np.random.default_rng(cfg.ref_seed)
     qs = np.sort(rng.choice(words.shape[0], size=min(sample, words.shape[0]), replace=False))
     want = oracle.count_batch(S, words[qs], lens[qs]).astype(np.uint32)
     assert np.array_equal(got[qs], want)
-    # every query certified against the (verified) suffix array
+    # every read certified against the (verified) suffix array
     nbad, first = oracle.certificate(S, sa_gpu, words, got, lens)
-    assert nbad == 0, f"{nbad} queries fail the certificate, first {first}"
+    assert nbad == 0, f"{nbad} reads fail the certificate, first {first}"
     return idx
 
 
@@ -308,3 +316,10 @@ def test_c3_full_size():
 @pytest.mark.slow
 def test_c4_full_size():
     _full_size_check(synth.CONFIGS["C4"], sample=256)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("m", [16, 150, 1000])
+def test_c5_read_lengths_full_reference(m):
+    # C5's reference (= C4's) at a sample of its read lengths; 2M reads per length
+    _full_size_check(synth.CONFIGS["C5"].with_m(m), sample=128, q_count=2_000_000)
