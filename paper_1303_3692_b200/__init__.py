@@ -234,22 +234,32 @@ class Index:
                                          int(chunk)), "sa_match_batch_host")
         return out
 
-    def locate(self, lohi, stream=None) -> Tuple["object", "object"]:
-        """Positions SA[lo..hi) of every query (SA order).  Returns (offsets int64 [Q+1], positions int32 [total])."""
+    def locate_offsets(self, lohi, stream=None):
+        """sa_locate_offsets: exclusive prefix sum of the counts (CUDA int64 [Q+1]); offsets[Q] = total."""
         import torch
         Q = lohi.shape[0]
-        dev = lohi.device
-        offsets = torch.empty(Q + 1, dtype=torch.int64, device=dev)
+        offsets = torch.empty(Q + 1, dtype=torch.int64, device=lohi.device)
         ws = _sz()
         _check(lib().sa_locate_workspace_size(Q, ctypes.byref(ws)), "sa_locate_workspace_size")
-        wsb = torch.empty(max(1, ws.value), dtype=torch.uint8, device=dev)
-        sp = _stream_ptr(stream)
-        _check(lib().sa_locate_offsets(self._h, _dptr(lohi), Q, _dptr(offsets), _dptr(wsb), ws.value, sp),
-               "sa_locate_offsets")
+        wsb = torch.empty(max(1, ws.value), dtype=torch.uint8, device=lohi.device)
+        _check(lib().sa_locate_offsets(self._h, _dptr(lohi), Q, _dptr(offsets), _dptr(wsb), ws.value,
+                                       _stream_ptr(stream)), "sa_locate_offsets")
+        return offsets
+
+    def locate_positions(self, lohi, offsets, n_reads: Optional[int] = None, stream=None):
+        """sa_locate over the first n_reads reads (default all): positions SA[lo..hi) in SA order, int32 [total]."""
+        import torch
+        Q = lohi.shape[0] if n_reads is None else int(n_reads)
         total = int(offsets[Q].item())
-        positions = torch.empty(total, dtype=torch.int32, device=dev)
-        _check(lib().sa_locate(self._h, _dptr(lohi), _dptr(offsets), Q, _dptr(positions), sp), "sa_locate")
-        return offsets, positions
+        positions = torch.empty(total, dtype=torch.int32, device=lohi.device)
+        _check(lib().sa_locate(self._h, _dptr(lohi), _dptr(offsets), Q, _dptr(positions), _stream_ptr(stream)),
+               "sa_locate")
+        return positions
+
+    def locate(self, lohi, stream=None) -> Tuple["object", "object"]:
+        """Positions SA[lo..hi) of every read (SA order).  Returns (offsets int64 [Q+1], positions int32 [total])."""
+        offsets = self.locate_offsets(lohi, stream)
+        return offsets, self.locate_positions(lohi, offsets, stream=stream)
 
 
 def random_gather(device: int = 0, buffer_bytes: int = 16 << 30, access_bytes: int = 32, n_threads: int = 148 * 2048 * 4,
