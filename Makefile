@@ -1,6 +1,6 @@
 # Build everything in-tree (the .so files travel to the GPU box with gpurun).
 NVCC      ?= /usr/local/cuda/bin/nvcc
-CC        ?= gcc
+CC        := gcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3,-Wall -Xptxas -v --expt-relaxed-constexpr
 CFLAGS    := -O2 -fPIC -fopenmp -Wall -Wextra

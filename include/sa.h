@@ -27,6 +27,10 @@
  *  T=3.  A query of m bases is packed 2 bits per base, MSB-first, into uint64
  *  words: base j of query q is at word q*stride_words + j/32, bits
  *  [63-2(j%32) .. 62-2(j%32)].  Bits past m are ignored.
+ *  Dense layout (stride_words = 0, fixed-length reads only: q_len = NULL,
+ *  fixed_len = m > 0): the reads are one continuous 2-bit stream, base j of
+ *  query q is stream base q*m + j (word (q*m+j)/32, same bit order); the buffer
+ *  holds ceil(Q*m/32) words.  25 bytes per 100-bp read instead of 32.
  *
  * What a match computes (Sec. IV; Alg. 1)
  * ----------------------------------------------------------------
@@ -125,7 +129,8 @@ sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
  *             that is 0).  With SA_MATCH_STATS its first 4*Q bytes receive the statistics.
  *   flags     0, or SA_MATCH_STATS and/or SA_MATCH_PRESORT (above).
  * Requirements: every length m <= 32*stride_words (longer lengths are clamped) and
- * m <= 65535.  Q == 0 is a no-op.  Errors: SA_EINVAL.  Asynchronous on `stream`. */
+ * m <= 65535; stride_words = 0 selects the dense layout (above).  Q == 0 is a no-op.
+ * Errors: SA_EINVAL.  Asynchronous on `stream`. */
 sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, uint32_t stride_words, uint32_t flags,
                                   size_t *bytes);
 sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,

@@ -102,6 +102,15 @@ def _dptr(t) -> Optional[int]:
     return None if t is None else (t.data_ptr() or None)
 
 
+def _rows(words, n_reads):
+    """(Q, stride_words): a 2-D [Q, stride] array is the strided layout; a 1-D stream with
+    n_reads given is the dense layout (stride_words = 0)."""
+    if n_reads is not None:
+        assert words.dim() == 1 if hasattr(words, "dim") else words.ndim == 1
+        return int(n_reads), 0
+    return int(words.shape[0]), int(words.shape[1])
+
+
 class Index:
     """Suffix-array index of one reference on one GPU (``sa_index_create``).
 
@@ -167,11 +176,12 @@ class Index:
         return ws.value
 
     def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None,
-              key_bases: int = 0, ordered_words=None, ordered_lens=None):
+              key_bases: int = 0, ordered_words=None, ordered_lens=None, n_reads: Optional[int] = None):
         """sa_match_order: a permutation of the reads sorted by their first key_bases bases (0 = 12);
-        optionally also the rows / lengths arranged in that order (for match(..., rows_ordered=True))."""
+        optionally also the rows / lengths arranged in that order (for match(..., rows_ordered=True)).
+        n_reads: give it (with a 1-D `words` stream and fixed_len) for the dense layout."""
         import torch
-        Q, stride = words.shape
+        Q, stride = _rows(words, n_reads)
         need = _sz()
         _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(need)), "sa_match_order_workspace_size")
         if workspace is None or workspace.numel() < need.value:
@@ -184,7 +194,8 @@ class Index:
         return out
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
-              presort: bool = False, workspace=None, order=None, rows_ordered: bool = False):
+              presort: bool = False, workspace=None, order=None, rows_ordered: bool = False,
+              n_reads: Optional[int] = None):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
@@ -192,13 +203,14 @@ class Index:
         presort: SA_MATCH_PRESORT (include/sa.h): order the reads inside the call.
         order: optional CUDA int32 [Q] permutation from order() (thread slot t takes read order[t]).
         rows_ordered: words/lens are order()'s ordered_words/ordered_lens (row t is read order[t]).
+        n_reads: with a 1-D `words` stream and fixed_len: the dense layout (include/sa.h).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [Q] of steps | text windows << 16 (SA_MATCH_STATS).
         """
         import torch
-        assert words.is_cuda and words.dtype == torch.int64 and words.dim() == 2 and words.is_contiguous()
-        Q, stride = words.shape
+        assert words.is_cuda and words.dtype == torch.int64 and words.is_contiguous()
+        Q, stride = _rows(words, n_reads)
         if lens is None and fixed_len is None:
             raise ValueError("give lens or fixed_len")
         if lens is not None:
@@ -219,7 +231,7 @@ class Index:
         return out
 
     def match_host(self, words: np.ndarray, lens: Optional[np.ndarray] = None, fixed_len: Optional[int] = None,
-                   out: Optional[np.ndarray] = None, chunk: int = 0) -> np.ndarray:
+                   out: Optional[np.ndarray] = None, chunk: int = 0, n_reads: Optional[int] = None) -> np.ndarray:
         """sa_match_batch_host: host buffers in (pinned recommended), intervals out; synchronous.
 
         words/lens/out may be numpy arrays or pinned CPU torch tensors (anything with .ctypes or .data_ptr())."""
@@ -227,7 +239,7 @@ class Index:
             if a is None:
                 return None
             return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
-        Q, stride = words.shape
+        Q, stride = _rows(words, n_reads)
         if out is None:
             out = np.empty((Q, 2), dtype=np.uint32)
         _check(lib().sa_match_batch_host(self._h, hptr(words), hptr(lens), int(fixed_len or 0), stride, Q, hptr(out),

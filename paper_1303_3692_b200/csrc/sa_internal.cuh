@@ -96,7 +96,7 @@ struct sa_index {
     uint32_t *pipe_lens[2] = {nullptr, nullptr};
     uint32_t *pipe_out[2] = {nullptr, nullptr};
     uint64_t pipe_chunk = 0;
-    uint32_t pipe_stride = 0;
+    uint64_t pipe_words_cap = 0;
 };
 
 // ---------------------------------------------------------------------------------------------

@@ -36,11 +36,23 @@ cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t s
 // ---- presort (SA_MATCH_PRESORT) ---------------------------------------------------------------
 // key = the read's first 16 bases (masked to its length), value = read index
 __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens,
-                               uint32_t fixed_len, uint32_t stride, uint64_t Q, uint32_t key_bases,
-                               uint32_t chunk_log2, uint32_t *__restrict__ keys, uint32_t *__restrict__ perm) {
+                               uint32_t fixed_len, uint32_t stride, uint64_t dense_words, uint64_t Q,
+                               uint32_t key_bases, uint32_t chunk_log2, uint32_t *__restrict__ keys,
+                               uint32_t *__restrict__ perm) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t m = min(lens ? __ldg(lens + q) : fixed_len, 32u * stride);
-        const uint64_t w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
+        uint32_t m;
+        uint64_t w0;
+        if (stride == 0) {  // dense layout: read q starts at bit 2*m*q of the stream
+            m = fixed_len;
+            const uint64_t bit = 2ull * m * q, i = bit >> 6;
+            const unsigned sh = (unsigned)(bit & 63);
+            const uint64_t lo = __ldg(reinterpret_cast<const unsigned long long *>(words) + i);
+            const uint64_t hi = (sh && i + 1 < dense_words) ? __ldg(reinterpret_cast<const unsigned long long *>(words) + i + 1) : 0ull;
+            w0 = sh ? (lo << sh) | (hi >> (64 - sh)) : lo;
+        } else {
+            m = min(lens ? __ldg(lens + q) : fixed_len, 32u * stride);
+            w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
+        }
         const uint32_t pre = (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases));
         keys[q] = chunk_log2 ? ((uint32_t)(q >> chunk_log2) << (2 * key_bases)) | pre : pre;
         perm[q] = (uint32_t)q;
@@ -107,7 +119,8 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     uint32_t cbits = 0;
     if (chunk_log2) while ((Q - 1) >> (chunk_log2 + cbits)) ++cbits;
     if (2 * key_bases + cbits > 32) cbits = 0;
-    k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, Q, key_bases,
+    const uint64_t dense_words = (Q * (uint64_t)fixed_len + 31) / 32;
+    k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
                                                      cbits ? chunk_log2 : 0u, keys_in, perm_in);
     SA_CUDA_TRY(cudaGetLastError());
     size_t b = L.cub_bytes;
@@ -145,9 +158,13 @@ sa_status check_match_args(const sa_index *idx, const uint64_t *q_words, const u
                            uint32_t stride, uint64_t Q, const uint32_t *out) {
     if (!idx) { sa_set_error("index is NULL"); return SA_EINVAL; }
     if (Q == 0) return SA_OK;
-    if (!q_words || !out) { sa_set_error("q_words/out_lohi NULL with Q=%llu", (unsigned long long)Q); return SA_EINVAL; }
-    if (stride == 0) { sa_set_error("stride_words must be >= 1"); return SA_EINVAL; }
-    if (!q_len && fixed_len > 32u * stride) {
+    if (!q_words || !out) { sa_set_error("q_words/out NULL with Q=%llu", (unsigned long long)Q); return SA_EINVAL; }
+    if (stride == 0) {  // dense layout
+        if (q_len || fixed_len == 0) {
+            sa_set_error("the dense layout (stride_words = 0) needs q_len = NULL and fixed_len > 0");
+            return SA_EINVAL;
+        }
+    } else if (!q_len && fixed_len > 32u * stride) {
         sa_set_error("fixed_len %u exceeds 32*stride_words = %u", fixed_len, 32u * stride);
         return SA_EINVAL;
     }
@@ -197,6 +214,10 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
     }
     SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace), L,
                        order, (cudaStream_t)stream));
+    if ((ordered_words || ordered_len) && stride_words == 0) {
+        sa_set_error("ordered rows are not available for the dense layout");
+        return SA_EINVAL;
+    }
     if (ordered_words || ordered_len) {
         const bool vec = stride_words == 4 && (reinterpret_cast<uintptr_t>(q_words) & 31) == 0 &&
                          (reinterpret_cast<uintptr_t>(ordered_words) & 31) == 0;
@@ -232,11 +253,13 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     // one vector load per read row when the row is exactly QW words and suitably aligned
     const uintptr_t wp = reinterpret_cast<uintptr_t>(q_words);
     a.vec_rows = (stride == 4 && (wp & 31) == 0) || (stride == 2 && (wp & 15) == 0);
+    a.dense_words = stride == 0 ? (Q * (uint64_t)fixed_len + 31) / 32 : 0;
     const bool st_on = stats != nullptr;
+    const uint32_t nw = stride ? stride : (fixed_len + 31) / 32;  // register words needed
     cudaError_t e;
-    if (stride <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
-    else if (stride <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
-    else if (stride <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
+    if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
+    else if (nw <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
+    else if (nw <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
     else e = launch_qw<0>(a, idx->layout, st_on, st);
     if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
     return SA_OK;
@@ -270,7 +293,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         order = perm;
     }
     const bool rows_ordered = (flags & SA_MATCH_ROWS_ORDERED) != 0;
-    if (rows_ordered && (!order || presort)) {
+    if (rows_ordered && (!order || presort || stride_words == 0)) {
         sa_set_error("SA_MATCH_ROWS_ORDERED needs the order the rows were arranged in");
         return SA_EINVAL;
     }
@@ -286,8 +309,12 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
     std::lock_guard<std::mutex> lock(idx->mu);
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     if (chunk_Q == 0) chunk_Q = 1ull << 22;
+    chunk_Q = (chunk_Q + 31) & ~31ull;  // dense layout: every chunk starts on a word boundary
     if (chunk_Q > Q) chunk_Q = Q;
-    if (idx->pipe_chunk < chunk_Q || idx->pipe_stride < stride) {
+    // words of `cq` reads starting at read q0 (q0 a multiple of chunk_Q, hence of 32 for dense)
+    auto words_of = [&](uint64_t cq) { return stride ? cq * stride : (cq * (uint64_t)fixed_len + 31) / 32; };
+    const uint64_t need_words = words_of(chunk_Q);
+    if (idx->pipe_chunk < chunk_Q || idx->pipe_words_cap < need_words) {
         for (int b = 0; b < 2; ++b) {
             cudaFree(idx->pipe_words[b]);
             cudaFree(idx->pipe_lens[b]);
@@ -297,14 +324,15 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             idx->pipe_out[b] = nullptr;
         }
         idx->pipe_chunk = 0;
+        idx->pipe_words_cap = 0;
         for (int b = 0; b < 2; ++b) {
             if (!idx->pipe_stream[b]) SA_CUDA_TRY(cudaStreamCreateWithFlags(&idx->pipe_stream[b], cudaStreamNonBlocking));
-            SA_CUDA_TRY(cudaMalloc(&idx->pipe_words[b], chunk_Q * stride * sizeof(uint64_t)));
+            SA_CUDA_TRY(cudaMalloc(&idx->pipe_words[b], need_words * sizeof(uint64_t)));
             SA_CUDA_TRY(cudaMalloc(&idx->pipe_lens[b], chunk_Q * sizeof(uint32_t)));
             SA_CUDA_TRY(cudaMalloc(&idx->pipe_out[b], chunk_Q * 2 * sizeof(uint32_t)));
         }
         idx->pipe_chunk = chunk_Q;
-        idx->pipe_stride = stride;
+        idx->pipe_words_cap = need_words;
     }
     // chunk c uses buffer set c%2 on stream c%2: H2D -> match -> D2H; the two streams overlap.
     uint64_t c = 0;
@@ -312,14 +340,16 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
         const int b = (int)(c & 1);
         cudaStream_t st = idx->pipe_stream[b];
         const uint64_t cq = std::min<uint64_t>(chunk_Q, Q - q0);
-        SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_words[b], q_words + q0 * stride, cq * stride * sizeof(uint64_t),
+        const uint64_t w0 = stride ? q0 * stride : q0 * (uint64_t)fixed_len / 32;
+        SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_words[b], q_words + w0, words_of(cq) * sizeof(uint64_t),
                                     cudaMemcpyHostToDevice, st));
         const uint32_t *dl = nullptr;
         if (q_len) {
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr, false, st));
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr,
+                            false, st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }

@@ -38,6 +38,7 @@ struct MatchArgs {
     uint32_t *__restrict__ stats;       // SA_MATCH_STATS
     const uint32_t *__restrict__ order; // thread slot t takes read order[t] (or t)
     bool vec_rows;                      // read rows can be loaded with one vector load (aligned, stride == QW)
+    uint64_t dense_words;               // stride == 0: dense layout, words = one 2-bit stream of this many words
     bool rows_ordered;                  // SA_MATCH_ROWS_ORDERED: row t is read order[t]
 };
 
@@ -69,6 +70,20 @@ struct QueryWords {
         for (int j = 0; j < QW; ++j)
             w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
     }
+    // dense layout: the read starts at bit `bit` of a continuous stream of `total` words
+    __device__ __forceinline__ void load_dense(const uint64_t *__restrict__ s, uint64_t bit, uint32_t nw,
+                                               uint64_t total) {
+        const uint64_t w0 = bit >> 6;
+        const unsigned sh = (unsigned)(bit & 63);
+        uint64_t r[QW + 1];
+#pragma unroll
+        for (int j = 0; j <= QW; ++j)
+            r[j] = (j <= (int)nw && w0 + j < total) ? __ldg(reinterpret_cast<const unsigned long long *>(s) + w0 + j)
+                                                    : 0ull;
+#pragma unroll
+        for (int j = 0; j < QW; ++j)
+            w[j] = j < (int)nw ? (sh ? (r[j] << sh) | (r[j + 1] >> (64 - sh)) : r[j]) : 0ull;
+    }
     __device__ __forceinline__ uint64_t first() const { return w[0]; }
     __device__ __forceinline__ uint64_t word(int j) const { return j < QW ? w[j] : 0ull; }
 };
@@ -76,11 +91,23 @@ template <>
 struct QueryWords<0> {
     const uint64_t *p;
     uint32_t nw;
+    unsigned sh = 0;     // dense layout: bit shift of the read inside its first word
+    uint64_t left = ~0ull;  // dense layout: words readable from p
     __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool) { p = q; nw = n; }
-    __device__ __forceinline__ uint64_t first() const { return __ldg(reinterpret_cast<const unsigned long long *>(p)); }
-    __device__ __forceinline__ uint64_t word(int j) const {
-        return (uint32_t)j < nw ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+    __device__ __forceinline__ void load_dense(const uint64_t *__restrict__ s, uint64_t bit, uint32_t n, uint64_t total) {
+        p = s + (bit >> 6);
+        sh = (unsigned)(bit & 63);
+        nw = n;
+        left = total - (bit >> 6);
     }
+    __device__ __forceinline__ uint64_t raw(uint64_t j) const {
+        return j < left ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+    }
+    __device__ __forceinline__ uint64_t word(int j) const {
+        if ((uint32_t)j >= nw) return 0ull;
+        return sh ? (raw(j) << sh) | (raw(j + 1) >> (64 - sh)) : raw(j);
+    }
+    __device__ __forceinline__ uint64_t first() const { return word(0); }
 };
 
 // ---- compare against the packed text --------------------------------------------------------
@@ -299,8 +326,15 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
 }
 
 __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
+    if (a.stride == 0) return a.fixed_len;  // dense layout: fixed length
     // lengths past the stride are clamped (include/sa.h requires m <= 32*stride_words)
     return min(a.lens ? __ldg(a.lens + q) : a.fixed_len, 32u * a.stride);
+}
+
+template <int QW>
+__device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint32_t m, QueryWords<QW> &P) {
+    if (a.stride == 0) P.load_dense(a.words, 2ull * m * row, (m + 31) >> 5, a.dense_words);
+    else P.load(a.words + row * a.stride, (m + 31) >> 5, a.vec_rows);
 }
 
 // One read per thread slot, all lanes of a warp in lock step (with sa_match_order the lanes hold
@@ -315,7 +349,7 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     const uint64_t row = a.rows_ordered ? t : q;                      // where its bases are
     const uint32_t m = read_len(a, row);
     QueryWords<QW> P;
-    P.load(a.words + row * a.stride, (m + 31) >> 5, a.vec_rows);
+    load_read<QW>(a, row, m, P);
     uint32_t lo, hi, steps = 0, texts = 0;
     search_read<QW, L>(a, P, m, lo, hi, steps, texts);
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here

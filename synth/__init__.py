@@ -53,12 +53,22 @@ def stride_for(m_max: int) -> int:
 
 def reads(ref: np.ndarray, q_count: int, m_min: int, m_max: int, p_random: float, p_mut_read: float,
           seed: int, q_begin: int = 0, stride: Optional[int] = None, nthreads: int = 0,
-          words_out: Optional[np.ndarray] = None, lens_out: Optional[np.ndarray] = None):
-    """Reads q_begin..q_begin+q_count-1: (words uint64[q_count, stride], lens uint32[q_count])."""
-    stride = stride or stride_for(m_max)
-    words = words_out if words_out is not None else np.empty((q_count, stride), dtype=np.uint64)
+          words_out: Optional[np.ndarray] = None, lens_out: Optional[np.ndarray] = None, dense: bool = False):
+    """Reads q_begin..q_begin+q_count-1: (words uint64[q_count, stride], lens uint32[q_count]).
+
+    dense=True (fixed length m only, q_count % 32 == 0): words is one continuous 2-bit stream of
+    q_count*m/32 words (include/sa.h "dense layout", stride_words = 0)."""
+    if dense:
+        assert m_min == m_max and q_count % 32 == 0
+        stride = 0
+        nwords = q_count // 32 * m_max
+        words = words_out if words_out is not None else np.empty(nwords, dtype=np.uint64)
+        assert words.dtype == np.uint64 and words.flags.c_contiguous and words.size >= nwords
+    else:
+        stride = stride or stride_for(m_max)
+        words = words_out if words_out is not None else np.empty((q_count, stride), dtype=np.uint64)
+        assert words.dtype == np.uint64 and words.flags.c_contiguous and words.size >= q_count * stride
     lens = lens_out if lens_out is not None else np.empty(q_count, dtype=np.uint32)
-    assert words.dtype == np.uint64 and words.flags.c_contiguous and words.size >= q_count * stride
     assert lens.dtype == np.uint32 and lens.size >= q_count
     ref = np.ascontiguousarray(ref, dtype=np.uint8)
     rc = _load().synth_reads(ref.ctypes.data if ref.size else None, ref.size, q_begin, q_count, m_min, m_max,
@@ -83,6 +93,19 @@ def pack_strings(seqs: Sequence[str], stride: Optional[int] = None):
         for j, ch in enumerate(s):
             words[q, j >> 5] |= np.uint64(_CODE[ch]) << np.uint64(62 - 2 * (j & 31))
     return words, lens
+
+
+def pack_dense(seqs: Sequence[str]) -> np.ndarray:
+    """Pack equal-length reads into the dense layout (one 2-bit stream, read i at bases [i*m, (i+1)*m))."""
+    m = len(seqs[0]) if seqs else 0
+    assert all(len(x) == m for x in seqs)
+    nbases = m * len(seqs)
+    words = np.zeros(max(1, (nbases + 31) // 32), dtype=np.uint64)
+    for i, x in enumerate(seqs):
+        for j, ch in enumerate(x.upper()):
+            b = i * m + j
+            words[b >> 5] |= np.uint64(_CODE[ch]) << np.uint64(62 - 2 * (b & 31))
+    return words
 
 
 def unpack_read(words_row: np.ndarray, m: int) -> str:

@@ -303,16 +303,22 @@ int synth_reference(int kind, uint64_t n, uint64_t seed, char *out, int nthreads
  * given one substitution at a uniform position with probability p_mut_read.
  * Writes packed words (stride words per read, zero beyond the read) and, if
  * lens != NULL, the length of each read.  Returns 0 or -1. */
+/* stride == 0 selects the dense layout (fixed length m_min == m_max == m only): read i occupies
+ * bases [i*m, (i+1)*m) of one continuous 2-bit stream; q_count must be a multiple of 32 so that
+ * every group of 32 reads covers exactly m whole words (groups are written by one thread). */
 int synth_reads(const char *ref, uint64_t n, uint64_t q_begin, uint64_t q_count, uint32_t m_min,
                 uint32_t m_max, double p_random, double p_mut_read, uint64_t seed, uint64_t *words,
                 uint32_t stride, uint32_t *lens, int nthreads) {
-    if (!words || m_min > m_max || (uint64_t)stride * 32 < m_max) return -1;
+    const int dense = stride == 0;
+    if (!words || m_min > m_max || (!dense && (uint64_t)stride * 32 < m_max)) return -1;
+    if (dense && (m_min != m_max || (q_count & 31) != 0)) return -1;
     if (n > 0 && !ref) return -1;
     set_threads(nthreads);
+    if (dense) memset(words, 0, (size_t)(q_count / 32 * m_max) * sizeof(uint64_t));
 #pragma omp parallel
     {
         char *buf = (char *)malloc(m_max + 1);
-#pragma omp for schedule(static)
+#pragma omp for schedule(static, 32)
         for (int64_t i = 0; i < (int64_t)q_count; ++i) {
             uint64_t q = q_begin + (uint64_t)i;
             rng_t r = rng_stream(seed, K_READ, q);
@@ -332,10 +338,18 @@ int synth_reads(const char *ref, uint64_t n, uint64_t q_begin, uint64_t q_count,
                     buf[j] = substitute(&r, buf[j]);
                 }
             }
-            uint64_t *w = words + (uint64_t)i * stride;
-            for (uint32_t t = 0; t < stride; ++t) w[t] = 0;
-            for (uint32_t j = 0; j < m; ++j)
-                w[j >> 5] |= (uint64_t)code_of(buf[j]) << (62 - 2 * (j & 31));
+            if (dense) {
+                const uint64_t b0 = (uint64_t)i * m;  /* base offset of this read in the stream */
+                for (uint32_t j = 0; j < m; ++j) {
+                    const uint64_t b = b0 + j;
+                    words[b >> 5] |= (uint64_t)code_of(buf[j]) << (62 - 2 * (b & 31));
+                }
+            } else {
+                uint64_t *w = words + (uint64_t)i * stride;
+                for (uint32_t t = 0; t < stride; ++t) w[t] = 0;
+                for (uint32_t j = 0; j < m; ++j)
+                    w[j >> 5] |= (uint64_t)code_of(buf[j]) << (62 - 2 * (j & 31));
+            }
             if (lens) lens[i] = m;
         }
         free(buf);

@@ -223,6 +223,25 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     assert torch.equal(got2, base)
 
 
+@pytest.mark.parametrize("m", [12, 31, 32, 100, 128, 150, 1000])
+def test_dense_layout_matches_strided(m):
+    ref = synth.reference(synth.REF_REPEAT, 1_000_000, 61)
+    Q = 4096 + 32 * 7
+    words, lens = synth.reads(ref, Q, m, m, 0.1, 0.05, 62)
+    dense, _ = synth.reads(ref, Q, m, m, 0.1, 0.05, 62, dense=True)
+    idx = sa.Index(ref, layout="rec32")
+    S = oracle.encode(ref)
+    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
+    d = torch.from_numpy(dense.view(np.int64)).cuda()
+    got = idx.match(d, None, fixed_len=m, n_reads=Q).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
+    perm = idx.order(d, None, fixed_len=m, n_reads=Q)
+    got2 = idx.match(d, None, fixed_len=m, n_reads=Q, order=perm).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got2, want)
+    got3 = idx.match_host(dense, None, fixed_len=m, n_reads=Q, chunk=1000)
+    assert np.array_equal(got3, want)
+
+
 def test_symbol_error_reports_position():
     with pytest.raises(sa.SAError) as e:
         sa.Index("ACGTACGTNACGT")

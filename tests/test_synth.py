@@ -57,3 +57,13 @@ def test_repeat_reference_has_repeats():
         return d
     iid = synth.reference(synth.REF_UNIFORM, 2_000_000, 3)
     assert dup20(ref) > 50 * max(1, dup20(iid))
+
+
+def test_dense_layout_equals_packed_strings():
+    ref = synth.reference(synth.REF_UNIFORM, 50_000, 2)
+    for m in (7, 32, 100):
+        w, l = synth.reads(ref, 96, m, m, 0.2, 0.0, 3)
+        d1, _ = synth.reads(ref, 96, m, m, 0.2, 0.0, 3, dense=True, nthreads=1)
+        d4, _ = synth.reads(ref, 96, m, m, 0.2, 0.0, 3, dense=True, nthreads=4)
+        want = synth.pack_dense([synth.unpack_read(w[i], m) for i in range(96)])
+        assert np.array_equal(d1, want[: d1.size]) and np.array_equal(d1, d4)
