@@ -37,8 +37,7 @@ cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t s
 // key = the read's first 16 bases (masked to its length), value = read index
 __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens,
                                uint32_t fixed_len, uint32_t stride, uint64_t dense_words, uint64_t Q,
-                               uint32_t key_bases, uint32_t chunk_log2, uint32_t *__restrict__ keys,
-                               uint32_t *__restrict__ perm) {
+                               uint32_t key_bases, uint32_t *__restrict__ keys, uint32_t *__restrict__ perm) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t m;
         uint64_t w0;
@@ -54,7 +53,7 @@ __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_
             w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
         }
         const uint32_t pre = (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases));
-        keys[q] = chunk_log2 ? ((uint32_t)(q >> chunk_log2) << (2 * key_bases)) | pre : pre;
+        keys[q] = pre;
         perm[q] = (uint32_t)q;
     }
 }
@@ -114,18 +113,13 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     uint32_t *perm_in = reinterpret_cast<uint32_t *>(ws + L.perm_in);
     uint64_t blocks = (Q + 255) / 256;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
-    // EXPERIMENT: SA_ORDER_CHUNK_LOG2=c orders reads within chunks of 2^c reads (chunk-major key)
-    static const uint32_t chunk_log2 = getenv("SA_ORDER_CHUNK_LOG2") ? (uint32_t)atoi(getenv("SA_ORDER_CHUNK_LOG2")) : 0u;
-    uint32_t cbits = 0;
-    if (chunk_log2) while ((Q - 1) >> (chunk_log2 + cbits)) ++cbits;
-    if (2 * key_bases + cbits > 32) cbits = 0;
     const uint64_t dense_words = (Q * (uint64_t)fixed_len + 31) / 32;
     k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
-                                                     cbits ? chunk_log2 : 0u, keys_in, perm_in);
+                                                     keys_in, perm_in);
     SA_CUDA_TRY(cudaGetLastError());
     size_t b = L.cub_bytes;
-    // key = [chunk |] the first key_bases bases: ceil(bits/8) radix passes
-    const int end_bit = 2 * (int)key_bases + (int)cbits;
+    // key = the first key_bases bases: ceil(2*key_bases/8) radix passes
+    const int end_bit = 2 * (int)key_bases;
     SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0,
                                                 end_bit, st));
     return SA_OK;
