@@ -23,6 +23,10 @@ $(PKG)/libsa.so: $(CU_SRCS) $(CU_HDRS)
 
 $(shell mkdir -p build)
 
+# A/B build variant: 128-bit instead of 256-bit record / read-row loads
+variants/libsa_load128.so: $(CU_SRCS) $(CU_HDRS)
+	mkdir -p variants && $(NVCC) $(NVFLAGS) -DSA_LOAD128 -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_load128.log || (cat build/ptxas_load128.log; false)
+
 clean:
 	rm -f synth/libsynth.so oracle/liboracle.so $(PKG)/libsa.so
 

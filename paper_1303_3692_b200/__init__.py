@@ -17,7 +17,8 @@ import numpy as np
 __all__ = ["SAError", "Index", "lib", "random_gather", "LIB_PATH", "EXPORTED_SYMBOLS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsa.so")
+# SA_LIB_PATH selects another build of the same library (A/B measurements of build variants)
+LIB_PATH = os.environ.get("SA_LIB_PATH") or os.path.join(_HERE, "libsa.so")
 
 SA_OK, SA_EINVAL, SA_ESYMBOL, SA_ETOOLONG, SA_ENOMEM, SA_ECUDA, SA_EEMPTY = 0, -1, -2, -3, -4, -5, -6
 SA_INDEX_PLAIN = 1          # sa_index_opts.flags: plain uint32 SA instead of 16-byte records

@@ -53,9 +53,15 @@ struct QueryWords {
     __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw, bool vec) {
         if constexpr (QW == 4) {
             if (vec) {
+#ifdef SA_LOAD128
+                const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2 *>(p));
+                const ulonglong2 y = __ldg(reinterpret_cast<const ulonglong2 *>(p) + 1);
+                w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
+#else
                 asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
                     : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
                     : "l"(p));
+#endif
                 return;
             }
         } else if constexpr (QW == 2) {
@@ -172,11 +178,17 @@ struct Rec {
     uint64_t c[kWords];  // c[j] = bases k+32j .. k+32j+31 (the last word holds 16)
     __device__ __forceinline__ void load(const uint4 *__restrict__ rec, uint64_t p) {
         if constexpr (L == L_REC32) {
-            // one 256-bit load (LDG.E.ENL2.256 on sm_100a): the whole 32-byte record, one sector
             uint64_t w0, w1, w2, w3;
+#ifdef SA_LOAD128
+            const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2 *>(rec + 2 * p));
+            const ulonglong2 y = __ldg(reinterpret_cast<const ulonglong2 *>(rec + 2 * p + 1));
+            w0 = x.x; w1 = x.y; w2 = y.x; w3 = y.y;
+#else
+            // one 256-bit load (LDG.E.ENL2.256 on sm_100a): the whole 32-byte record, one sector
             asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
                 : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
                 : "l"(rec + 2 * p));
+#endif
             sa = (uint32_t)w0;
             c[0] = w1;
             c[1] = w2;
@@ -248,25 +260,44 @@ __device__ __forceinline__ void compare_rec(const MatchArgs &a, const Rec<L> &r,
     else { sign = 1; lcp = (uint32_t)len; }          // the suffix is a proper prefix of P (reading A7)
 }
 
-// Probe pivot p: sign(P - t_SA[p]) and lcp.  in_bracket: P has >= k bases and (L, R) lies inside
-// its k-mer bracket, so a record's cache applies.
+// A probe of pivot p, split into its load (issued early) and its compare (sign(P - t_SA[p]), lcp).
+// in_bracket: P has >= k bases and the pivot lies inside its k-mer bracket, so a record's cache applies.
+template <int L>
+struct Probe {
+    Rec<L> r;
+    __device__ __forceinline__ void load(const MatchArgs &a, uint64_t p) { r.load(a.rec, p); }
+    __device__ __forceinline__ uint64_t sa() const { return r.sa; }
+};
+template <>
+struct Probe<L_PLAIN> {
+    uint64_t s;
+    __device__ __forceinline__ void load(const MatchArgs &a, uint64_t p) { s = __ldg(a.sa + p); }
+    __device__ __forceinline__ uint64_t sa() const { return s; }
+};
+
+template <int QW, int L>
+__device__ __forceinline__ void compare_probe(const MatchArgs &a, const Probe<L> &pr, const QueryWords<QW> &P,
+                                              uint32_t m, uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp,
+                                              uint32_t &texts) {
+    if constexpr (L == L_PLAIN) {
+        ++texts;
+        compare_text<QW>(a.text, a.n, pr.s, P, m, skip, sign, lcp);
+    } else {
+        if (in_bracket) {
+            compare_rec<QW, L>(a, pr.r, P, m, skip, sign, lcp, texts);
+        } else {
+            ++texts;
+            compare_text<QW>(a.text, a.n, pr.r.sa, P, m, skip, sign, lcp);
+        }
+    }
+}
+
 template <int QW, int L>
 __device__ __forceinline__ void probe(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint64_t p,
                                       uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts) {
-    if constexpr (L == L_PLAIN) {
-        const uint64_t s = __ldg(a.sa + p);
-        ++texts;
-        compare_text<QW>(a.text, a.n, s, P, m, skip, sign, lcp);
-    } else {
-        Rec<L> r;
-        r.load(a.rec, p);
-        if (in_bracket) {
-            compare_rec<QW, L>(a, r, P, m, skip, sign, lcp, texts);
-        } else {
-            ++texts;
-            compare_text<QW>(a.text, a.n, r.sa, P, m, skip, sign, lcp);
-        }
-    }
+    Probe<L> pr;
+    pr.load(a, p);
+    compare_probe<QW, L>(a, pr, P, m, skip, in_bracket, sign, lcp, texts);
 }
 
 // Binary search over (Lp1-1, R): LB rule (lower: R moves when P <= t) or RB rule (R moves when P < t).
@@ -310,19 +341,52 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
     uint32_t Lp1, R;
     table_pair(a.table, x, Lp1, R);
     uint32_t lcpL = 0, lcpR = 0;
-    uint32_t sLp1 = 0, sR = 0, slcpR = 0;
+    uint32_t hLp1 = 0, hR = 0, hlcpL = 0, hlcpR = 0;
     bool split = false;
-    while (R > Lp1) {  // LB rule, remembering the first pivot where P is a prefix of the suffix
+    while (R > Lp1) {  // LB rule until the first pivot where P is a prefix of the suffix (the split)
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
         probe<QW, L>(a, P, m, p, min(lcpL, lcpR), true, sign, lcp, texts);
         ++steps;
-        if (sign == 0 && !split) { split = true; sLp1 = p + 1; sR = R; slcpR = lcpR; }
-        if (sign <= 0) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+        if (sign == 0) {  // lo lies in (L, p], hi in (p, R]: the RB search starts from here
+            split = true;
+            hLp1 = p + 1; hR = R; hlcpL = lcp; hlcpR = lcpR;
+            R = p; lcpR = lcp;
+            break;
+        }
+        if (sign < 0) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+    }
+    if (!split) {  // no suffix has P as a prefix: an empty interval at the insertion point
+        lo = hi = R;
+        return;
+    }
+    // the LB search (lower half) and the RB search (upper half) are independent: both probes of an
+    // iteration are issued before either compare, so a repeat's two chains overlap in memory
+    while (R > Lp1 || hR > hLp1) {
+        const bool A = R > Lp1, B = hR > hLp1;
+        const uint32_t pa = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
+        const uint32_t pb = (uint32_t)(((uint64_t)hLp1 - 1 + hR) >> 1);
+        Probe<L> ra, rb;
+        if (A) ra.load(a, pa);
+        if (B) rb.load(a, pb);
+        if (A) {
+            int sign;
+            uint32_t lcp;
+            compare_probe<QW, L>(a, ra, P, m, min(lcpL, lcpR), true, sign, lcp, texts);
+            ++steps;
+            if (sign <= 0) { R = pa; lcpR = lcp; } else { Lp1 = pa + 1; lcpL = lcp; }
+        }
+        if (B) {
+            int sign;
+            uint32_t lcp;
+            compare_probe<QW, L>(a, rb, P, m, min(hlcpL, hlcpR), true, sign, lcp, texts);
+            ++steps;
+            if (sign < 0) { hR = pb; hlcpR = lcp; } else { hLp1 = pb + 1; hlcpL = lcp; }
+        }
     }
     lo = R;
-    hi = split ? bound<QW, L>(a, P, m, sLp1, sR, m, slcpR, false, true, steps, texts) : lo;
+    hi = hR;
 }
 
 __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
