@@ -23,11 +23,17 @@ $(PKG)/libsa.so: $(CU_SRCS) $(CU_HDRS)
 
 $(shell mkdir -p build)
 
-# A/B build variant: 128-bit instead of 256-bit record / read-row loads
-variants/libsa_load128.so: $(CU_SRCS) $(CU_HDRS)
-	mkdir -p variants && $(NVCC) $(NVFLAGS) -DSA_LOAD128 -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_load128.log || (cat build/ptxas_load128.log; false)
+# A/B build variants (variants/*.so; bench.py / tests load one with SA_LIB_PATH=...)
+VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ldca.so variants/libsa_seqhi.so
+variants/libsa_ldcg.so: DEFS := -DSA_LD_MODE=1
+variants/libsa_ldnoalloc.so: DEFS := -DSA_LD_MODE=2
+variants/libsa_ldca.so: DEFS := -DSA_LD_MODE=3
+variants/libsa_seqhi.so: DEFS := -DSA_SEQ_HI
+variants: $(VARIANTS)
+variants/%.so: $(CU_SRCS) $(CU_HDRS)
+	mkdir -p variants && $(NVCC) $(NVFLAGS) $(DEFS) -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_$(notdir $@).log || (cat build/ptxas_$(notdir $@).log; false)
 
 clean:
 	rm -f synth/libsynth.so oracle/liboracle.so $(PKG)/libsa.so
 
-.PHONY: all clean
+.PHONY: all clean variants

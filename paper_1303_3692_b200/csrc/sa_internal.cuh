@@ -102,12 +102,50 @@ struct sa_index {
 // ---------------------------------------------------------------------------------------------
 // device helpers
 
+// Loads of the search path.  SA_LD_MODE (compile time) selects the PTX cache operator for every
+// random access of the match kernel: 0 = ld.global.nc (read-only path, default), 1 = ld.global.cg
+// (L2 only), 2 = ld.global.nc.L1::no_allocate, 3 = ld.global.ca.
+#ifndef SA_LD_MODE
+#define SA_LD_MODE 0
+#endif
+#if SA_LD_MODE == 1
+#define SA_LD_OP "ld.global.cg"
+#elif SA_LD_MODE == 2
+#define SA_LD_OP "ld.global.nc.L1::no_allocate"
+#elif SA_LD_MODE == 3
+#define SA_LD_OP "ld.global.ca"
+#else
+#define SA_LD_OP "ld.global.nc"
+#endif
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t *p) {
+    uint32_t v;
+    asm(SA_LD_OP ".u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_u64(const uint64_t *p) {
+    uint64_t v;
+    asm(SA_LD_OP ".u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_v4u32(const void *p) {
+    uint4 v;
+    asm(SA_LD_OP ".v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void ld_v2u64(const void *p, uint64_t &a, uint64_t &b) {
+    asm(SA_LD_OP ".v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+// 256-bit load (sm_100): LDG.E.ENL2.256
+__device__ __forceinline__ void ld_v4u64(const void *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
+    asm(SA_LD_OP ".v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
 // 32 bases of the packed text starting at base b (b < n + 32); bases past n read as 0 ('a').
 __device__ __forceinline__ uint64_t text_window(const uint64_t *__restrict__ text, uint64_t b) {
     const uint64_t w = b >> 5;
     const unsigned sh = (unsigned)(b & 31u) << 1;
-    const uint64_t x0 = __ldg(reinterpret_cast<const unsigned long long *>(text) + w);
-    const uint64_t x1 = __ldg(reinterpret_cast<const unsigned long long *>(text) + w + 1);
+    const uint64_t x0 = ld_u64(text + w);
+    const uint64_t x1 = ld_u64(text + w + 1);
     return sh ? (x0 << sh) | (x1 >> (64u - sh)) : x0;
 }
 

@@ -53,28 +53,18 @@ struct QueryWords {
     __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw, bool vec) {
         if constexpr (QW == 4) {
             if (vec) {
-#ifdef SA_LOAD128
-                const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2 *>(p));
-                const ulonglong2 y = __ldg(reinterpret_cast<const ulonglong2 *>(p) + 1);
-                w[0] = x.x; w[1] = x.y; w[2] = y.x; w[3] = y.y;
-#else
-                asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
-                    : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
-                    : "l"(p));
-#endif
+                ld_v4u64(p, w[0], w[1], w[2], w[3]);
                 return;
             }
         } else if constexpr (QW == 2) {
             if (vec) {
-                const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2 *>(p));
-                w[0] = v.x;
-                w[1] = v.y;
+                ld_v2u64(p, w[0], w[1]);
                 return;
             }
         }
 #pragma unroll
         for (int j = 0; j < QW; ++j)
-            w[j] = (j < (int)nw) ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+            w[j] = (j < (int)nw) ? ld_u64(p + j) : 0ull;
     }
     // dense layout: the read starts at bit `bit` of a continuous stream of `total` words
     __device__ __forceinline__ void load_dense(const uint64_t *__restrict__ s, uint64_t bit, uint32_t nw,
@@ -84,8 +74,7 @@ struct QueryWords {
         uint64_t r[QW + 1];
 #pragma unroll
         for (int j = 0; j <= QW; ++j)
-            r[j] = (j <= (int)nw && w0 + j < total) ? __ldg(reinterpret_cast<const unsigned long long *>(s) + w0 + j)
-                                                    : 0ull;
+            r[j] = (j <= (int)nw && w0 + j < total) ? ld_u64(s + w0 + j) : 0ull;
 #pragma unroll
         for (int j = 0; j < QW; ++j)
             w[j] = j < (int)nw ? (sh ? (r[j] << sh) | (r[j + 1] >> (64 - sh)) : r[j]) : 0ull;
@@ -107,7 +96,7 @@ struct QueryWords<0> {
         left = total - (bit >> 6);
     }
     __device__ __forceinline__ uint64_t raw(uint64_t j) const {
-        return j < left ? __ldg(reinterpret_cast<const unsigned long long *>(p) + j) : 0ull;
+        return j < left ? ld_u64(p + j) : 0ull;
     }
     __device__ __forceinline__ uint64_t word(int j) const {
         if ((uint32_t)j >= nw) return 0ull;
@@ -179,23 +168,15 @@ struct Rec {
     __device__ __forceinline__ void load(const uint4 *__restrict__ rec, uint64_t p) {
         if constexpr (L == L_REC32) {
             uint64_t w0, w1, w2, w3;
-#ifdef SA_LOAD128
-            const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2 *>(rec + 2 * p));
-            const ulonglong2 y = __ldg(reinterpret_cast<const ulonglong2 *>(rec + 2 * p + 1));
-            w0 = x.x; w1 = x.y; w2 = y.x; w3 = y.y;
-#else
             // one 256-bit load (LDG.E.ENL2.256 on sm_100a): the whole 32-byte record, one sector
-            asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
-                : "=l"(w0), "=l"(w1), "=l"(w2), "=l"(w3)
-                : "l"(rec + 2 * p));
-#endif
+            ld_v4u64(rec + 2 * p, w0, w1, w2, w3);
             sa = (uint32_t)w0;
             c[0] = w1;
             c[1] = w2;
             c[2] = w3;
             c[3] = w0 & 0xFFFFFFFF00000000ull;
         } else {
-            const uint4 a = __ldg(rec + p);
+            const uint4 a = ld_v4u32(rec + p);
             sa = a.x;
             c[0] = ((uint64_t)a.w << 32) | a.z;
             c[1] = (uint64_t)a.y << 32;
@@ -205,12 +186,12 @@ struct Rec {
 
 // T[x] and T[x+1]: one aligned 16-byte load unless x sits in the last slot of its 16-byte group.
 __device__ __forceinline__ void table_pair(const uint32_t *__restrict__ T, uint64_t x, uint32_t &a, uint32_t &b) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(T + (x & ~3ull)));
+    const uint4 v = ld_v4u32(T + (x & ~3ull));
     switch (x & 3) {
     case 0: a = v.x; b = v.y; break;
     case 1: a = v.y; b = v.z; break;
     case 2: a = v.z; b = v.w; break;
-    default: a = v.w; b = __ldg(T + x + 1); break;
+    default: a = v.w; b = ld_u32(T + x + 1); break;
     }
 }
 
@@ -271,7 +252,7 @@ struct Probe {
 template <>
 struct Probe<L_PLAIN> {
     uint64_t s;
-    __device__ __forceinline__ void load(const MatchArgs &a, uint64_t p) { s = __ldg(a.sa + p); }
+    __device__ __forceinline__ void load(const MatchArgs &a, uint64_t p) { s = ld_u32(a.sa + p); }
     __device__ __forceinline__ uint64_t sa() const { return s; }
 };
 
@@ -330,8 +311,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
         // lo in [T[xa]-(k-m), T[xa]], hi in [T[xb]-(k-1), T[xb]], xa = x.a^(k-m), xb = (x+1).a^(k-m)
         // (DESIGN.md "Bracket, short reads"); each searched over (T[.]-k-1, T[.])
         const uint64_t x = P.first() >> (64 - 2 * m);
-        const uint32_t Ta = __ldg(a.table + (x << (2 * (k - m))));
-        const uint32_t Tb = __ldg(a.table + ((x + 1) << (2 * (k - m))));
+        const uint32_t Ta = ld_u32(a.table + (x << (2 * (k - m))));
+        const uint32_t Tb = ld_u32(a.table + ((x + 1) << (2 * (k - m))));
         lo = bound<QW, L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts);
         hi = bound<QW, L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts);
         return;
@@ -361,6 +342,12 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
         lo = hi = R;
         return;
     }
+#ifdef SA_SEQ_HI
+    // A/B variant: finish the LB search, then run the RB search
+    lo = bound<QW, L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts);
+    hi = bound<QW, L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts);
+    return;
+#endif
     // the LB search (lower half) and the RB search (upper half) are independent: both probes of an
     // iteration are issued before either compare, so a repeat's two chains overlap in memory
     while (R > Lp1 || hR > hLp1) {
