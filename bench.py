@@ -143,23 +143,16 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def algorithmic_bytes_per_query(n, k, m, layout="rec32"):
-    """the sector-granular bytes the k-mer-bracket joint search must move per read.
+def algorithmic_bytes_per_query(layout, m, probes, text_windows):
+    """sector-granular bytes of the accesses the search itself makes per read.
 
-    D = log2(mean bracket + 1) + 1 search steps (one descent plus on average one extra level for
-    the hi continuation); every random access moves one 32-B sector.
-      plain : 1 table sector + D x (SA sector + text sector)                      + read + result
-      rec16 : 1 table sector + D x (record sector) + 1 text sector (bases past 48) + read + result
-      rec32 : 1 table sector + D x (record sector) [+ 1 text sector if m > k+112]  + read + result
-    read = one 32-B sector per read gathered through the ordering (ceil(m/4) B for m > 128),
-    result = 8 B."""
-    bracket = n / float(4 ** k)
-    D = math.log2(bracket + 1.0) + 1.0
+    Every random access moves one 32-B sector: the bracket-table pair (1), one record / SA entry per
+    probe, one per text window (plain: every probe; rec16: the bases past the 48 cached ones), the
+    read row (32 B, gathered through the ordering; ceil(m/4) B beyond 128 bases) and the 8-B result.
+    `probes` and `text_windows` are the per-read means counted by the SA_MATCH_STATS launch on this
+    very batch, so the figure is the algorithm's own access count on the workload, not a cache model."""
     read = max(32.0, math.ceil(m / 4.0))
-    if layout == "plain":
-        return 32.0 + D * 64.0 + read + 8.0
-    text = 32.0 if (layout == "rec16" and m > k + 48) or (layout == "rec32" and m > k + 112) else 0.0
-    return 32.0 + D * 32.0 + text + read + 8.0
+    return 32.0 + 32.0 * probes + 32.0 * text_windows + read + 8.0
 
 
 def traffic_per_launch(workload_name):
@@ -333,21 +326,15 @@ def main():
     value = total_reads / (elapsed_ms * 1e-3)
     ms_per_step = elapsed_ms / args.steps
 
-    # ---- roofline of the dominant (only) kernel: k_match ----
     m_alg = cfg.m_max if fixed else (cfg.m_min + cfg.m_max) / 2
-    bpq = algorithmic_bytes_per_query(cfg.n, idx.k, m_alg, args.layout)
     avg_launch_s = statistics.mean(launch_ms) * 1e-3
-    achieved = bpq * Q / avg_launch_s / 1e9
     peak, peak_src = measured_peaks()
-    traffic = traffic_per_launch(cfg.name)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_match", "algorithmic_bytes_per_query": bpq,
-                "peak_source": peak_src}
+    traffic = traffic_per_launch(f"{cfg.name}/{args.layout}")
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
-            "roofline": roofline, "clocks": sampler.result(),
+            "clocks": sampler.result(),
             "gpu_launches": args.steps * (2 if presort else 1),
             "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
                                           if presort else 0),
@@ -371,6 +358,18 @@ def main():
     line["search_stats"] = {"mean_steps": float(steps_t.mean()), "mean_text_windows": float(texts_t.mean()),
                             "p99_steps": float(torch.quantile(steps_t[:1 << 20], 0.99)),
                             "max_steps": float(steps_t.max())}
+
+    # ---- roofline of the dominant kernel (k_match; the ordering sort is CUB's) ----
+    bpq = algorithmic_bytes_per_query(args.layout, m_alg, line["search_stats"]["mean_steps"],
+                                      line["search_stats"]["mean_text_windows"])
+    achieved = bpq * Q / avg_launch_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "k_match", "algorithmic_bytes_per_query": bpq,
+                "peak_source": peak_src}
+    if traffic:
+        roofline["traffic_GBps"] = traffic / avg_launch_s / 1e9
+        roofline["traffic_frac"] = roofline["traffic_GBps"] / peak
+    line["roofline"] = roofline
     del st, chk
 
     # ---- locate (separate call): positions SA[lo..hi) of the reads ----
