@@ -435,7 +435,31 @@ def main():
         line["e2e"] = {"value": Q * world * e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": Q * 8, "steps": e2e_steps,
                        "layout": "dense 2-bit stream" if dense else f"{stride} words per read",
-                       "path": "sa_match_batch_host (pinned host buffers, 2 streams, 4M-read chunks)"}
+                       "path": "sa_match_batch_host (pinned host buffers, 2 streams, 4M-read chunks)",
+                       "overlapped_ms_per_step": dt * 1e3 / e2e_steps}
+        # the paper's Table V split (input / kernel / output time), measured one phase at a
+        # time without overlap: H2D of the reads, ordering + search on the device copy, D2H of the intervals
+        if dense:
+            ev3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            dwd = torch.empty(nwords, dtype=torch.int64, device=dev)
+            outd = torch.empty((Q, 2), dtype=torch.int32, device=dev)
+            permd = torch.empty(Q, dtype=torch.int32, device=dev)
+            torch.cuda.synchronize()
+            ev3[0].record(stream)
+            dwd.copy_(dw, non_blocking=True)
+            ev3[1].record(stream)
+            idx.order(dwd, None, fixed_len=fixed, out=permd, stream=stream, workspace=ws, key_bases=args.order_bases,
+                      n_reads=Q)
+            idx.match(dwd, None, fixed_len=fixed, out=outd, stream=stream, workspace=ws, order=permd, n_reads=Q)
+            ev3[2].record(stream)
+            out_h.copy_(outd, non_blocking=True)
+            ev3[3].record(stream)
+            torch.cuda.synchronize()
+            if not torch.equal(outd.cpu(), out.cpu()):
+                raise RuntimeError("dense-layout device path disagrees with the strided path")
+            line["e2e"]["split_ms"] = {"input": ev3[0].elapsed_time(ev3[1]), "kernel": ev3[1].elapsed_time(ev3[2]),
+                                       "output": ev3[2].elapsed_time(ev3[3])}
+            del dwd, outd, permd
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -68,7 +68,7 @@ typedef enum {
 typedef struct {
     int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device */
     uint32_t kmer_k;   /* k of the k-mer bracket table, 1..16; 0 = auto (min(16, floor(log4 n) + 1)) */
-    uint32_t flags;    /* 0, SA_INDEX_PLAIN or SA_INDEX_REC32 */
+    uint32_t flags;    /* 0, SA_INDEX_PLAIN or SA_INDEX_REC32, optionally | SA_INDEX_BUILD_DC3 */
     uint32_t reserved; /* must be 0 */
 } sa_index_opts;
 
@@ -79,6 +79,10 @@ typedef struct {
  * SA (4 B x n); every step also reads the packed text. */
 #define SA_INDEX_PLAIN 1u
 #define SA_INDEX_REC32 2u
+/* sa_index_opts.flags: build the suffix array with the paper's DC3 / skew algorithm (P:L105-150,
+ * Sec. III; on the GPU: radix-sorted sample triples, recursion on the reduced string, merge-path
+ * merge) instead of the default prefix doubling.  Same SA (it is unique); a different build cost. */
+#define SA_INDEX_BUILD_DC3 4u
 
 /* sa_match_batch flags. */
 #define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace:
@@ -171,11 +175,18 @@ sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_
 /* Measurement tool (not on the path): random-access gather rate of the
  * device's memory.  Allocates buffer_bytes, then every thread issues `loads`
  * independent (dependent=0) or pointer-chased (dependent=1) loads -- or, with dependent=2,
- * independent stores -- of
+ * independent stores; 10..13: independent loads with the PTX cache operator .nc / .cg / .cv /
+ * .nc.L1::no_allocate (access_bytes 8 or 32) -- of
  * access_bytes (4, 8, 16 or 32) at hashed, access_bytes-aligned offsets.
  * *ms = device time of one launch of n_threads threads (CUDA events). */
 sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,
                                 uint32_t loads, int32_t dependent, float *ms);
+
+/* DC3 trace for checking the build against the paper's worked example (Tables II-III,
+ * P:L112-128): runs DC3 on ref_ascii[0..n) on the current device and returns, on the host,
+ * sample_rank[i] = the 1-based rank of S_i among the sample suffixes (i mod 3 != 0; 0 for i mod 3 = 0)
+ * and nonsample[0..ceil(n/3)) = the B_0 positions in suffix order (DC3 step 2).  Either may be NULL. */
+sa_status sa_dc3_trace(const char *ref_ascii, uint64_t n, uint32_t *sample_rank, uint32_t *nonsample);
 
 /* Thread-local detail of the last failure on this thread ("" if none). */
 const char *sa_last_error(void);

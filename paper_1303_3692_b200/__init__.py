@@ -26,6 +26,7 @@ SA_INDEX_REC32 = 2          # sa_index_opts.flags: 32-byte records caching 112 b
 SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windows << 16 into the workspace
 SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 12 bases before the search
 SA_MATCH_ROWS_ORDERED = 8   # sa_match_batch flags: rows already arranged in `order` order
+SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 LAYOUTS = {"rec16": 0, "rec32": SA_INDEX_REC32, "plain": SA_INDEX_PLAIN}
 _NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
           -6: "SA_EEMPTY"}
@@ -56,6 +57,7 @@ _SIGS = {
     "sa_locate_offsets": ([_p, _p, _u64, _p, _p, _sz, _p], ctypes.c_int),
     "sa_locate": ([_p, _p, _p, _u64, _p, _p], ctypes.c_int),
     "sa_tool_random_gather": ([_i32, _u64, _u32, _u64, _u32, _i32, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+    "sa_dc3_trace": ([_p, _u64, _p, _p], ctypes.c_int),
     "sa_last_error": ([], ctypes.c_char_p),
     "sa_version": ([], ctypes.c_int32),
 }
@@ -118,14 +120,18 @@ class Index:
     ref: str / bytes / numpy uint8 array of ACGT (case-insensitive).  k: bracket-table k (0 = auto).
     layout: "rec16" (default, 16-byte records caching 48 bases), "rec32" (32-byte records, 112 bases)
     or "plain" (uint32 SA; every step reads the packed text).
+    build: "doubling" (default, prefix doubling) or "dc3" (the paper's DC3, SA_INDEX_BUILD_DC3).
     """
 
-    def __init__(self, ref, k: int = 0, device: Optional[int] = None, layout: str = "rec16"):
+    def __init__(self, ref, k: int = 0, device: Optional[int] = None, layout: str = "rec16", build: str = "doubling"):
         if isinstance(ref, str):
             ref = ref.encode("ascii")
         arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
             np.ascontiguousarray(ref, dtype=np.uint8)
-        opts = _Opts(-1 if device is None else int(device), int(k), LAYOUTS[layout], 0)
+        if build not in ("doubling", "dc3"):
+            raise ValueError("build must be 'doubling' or 'dc3'")
+        flags = LAYOUTS[layout] | (SA_INDEX_BUILD_DC3 if build == "dc3" else 0)
+        opts = _Opts(-1 if device is None else int(device), int(k), flags, 0)
         self.layout = layout
         h = _p()
         _check(lib().sa_index_create(arr.ctypes.data if arr.size else None, arr.size, ctypes.byref(opts),
@@ -273,6 +279,19 @@ class Index:
         """Positions SA[lo..hi) of every read (SA order).  Returns (offsets int64 [Q+1], positions int32 [total])."""
         offsets = self.locate_offsets(lohi, stream)
         return offsets, self.locate_positions(lohi, offsets, stream=stream)
+
+
+def dc3_trace(ref):
+    """sa_dc3_trace: (sample_rank uint32[n], nonsample uint32[ceil(n/3)]) of the paper's DC3 steps 1-2."""
+    if isinstance(ref, str):
+        ref = ref.encode("ascii")
+    arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
+        np.ascontiguousarray(ref, dtype=np.uint8)
+    n = arr.size
+    rank = np.empty(n, dtype=np.uint32)
+    b0 = np.empty((n + 2) // 3, dtype=np.uint32)
+    _check(lib().sa_dc3_trace(arr.ctypes.data, n, rank.ctypes.data, b0.ctypes.data), "sa_dc3_trace")
+    return rank, b0
 
 
 def random_gather(device: int = 0, buffer_bytes: int = 16 << 30, access_bytes: int = 32, n_threads: int = 148 * 2048 * 4,

@@ -52,8 +52,8 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     }
     sa_index_opts o{-1, 0, 0, 0};
     if (opts) o = *opts;
-    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32)) != 0 || o.flags == (SA_INDEX_PLAIN | SA_INDEX_REC32) ||
-        o.reserved != 0) {
+    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32 | SA_INDEX_BUILD_DC3)) != 0 ||
+        (o.flags & (SA_INDEX_PLAIN | SA_INDEX_REC32)) == (SA_INDEX_PLAIN | SA_INDEX_REC32) || o.reserved != 0) {
         sa_set_error("unknown opts.flags bits / reserved must be 0");
         return SA_EINVAL;
     }
@@ -77,6 +77,7 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     idx->device = dev;
     idx->n = n;
     idx->layout = (o.flags & SA_INDEX_PLAIN) ? 0 : (o.flags & SA_INDEX_REC32) ? 2 : 1;
+    idx->build_dc3 = (o.flags & SA_INDEX_BUILD_DC3) != 0;
     uint32_t k = o.kmer_k;
     if (k == 0) {  // auto: floor(log4 n) + 1 (mean bracket < 1 suffix), at most 16 (a 16 GiB table)
         k = 1;
@@ -106,6 +107,30 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
 }
 
 extern "C" void sa_index_destroy(sa_index *idx) { free_index(idx); }
+
+extern "C" sa_status sa_dc3_trace(const char *ref_ascii, uint64_t n, uint32_t *sample_rank, uint32_t *nonsample) {
+    sa_clear_error();
+    if (!ref_ascii || n == 0) { sa_set_error("empty or NULL reference"); return SA_EINVAL; }
+    if (n > 0xFFFFFFFFull) { sa_set_error("reference too long"); return SA_ETOOLONG; }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        (void)cudaGetLastError();
+        sa_set_error("no CUDA device available");
+        return SA_ECUDA;
+    }
+    sa_index *idx = new (std::nothrow) sa_index();
+    if (!idx) return SA_ENOMEM;
+    SA_CUDA_TRY(cudaGetDevice(&idx->device));
+    idx->n = n;
+    cudaStream_t st = nullptr;
+    sa_status s = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess ? SA_OK : SA_ECUDA;
+    if (s == SA_OK) s = sa_pack_text(idx, ref_ascii, st);
+    if (s == SA_OK && cudaMalloc(&idx->sa, n * sizeof(uint32_t)) != cudaSuccess) { (void)cudaGetLastError(); s = SA_ENOMEM; }
+    if (s == SA_OK) s = sa_build_sa_dc3(idx, st, sample_rank, nonsample);
+    if (st) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
+    free_index(idx);
+    return s;
+}
 
 extern "C" sa_status sa_index_info(const sa_index *idx, uint64_t *n, uint32_t *kmer_k, uint64_t *device_bytes,
                                    int32_t *device) {
@@ -185,6 +210,43 @@ __global__ void k_gather(const uint8_t *__restrict__ buf, uint64_t slot_mask, ui
     if (acc == 0x5eed) sink[0] = acc;  // keeps the loads alive
 }
 
+// modes 10..13: independent random loads with an explicit PTX cache operator (measurement of the
+// DRAM bytes one random access costs): 10 ld.global.nc, 11 ld.global.cg, 12 ld.global.cv,
+// 13 ld.global.nc.L1::no_allocate; BYTES = 8 or 32.
+template <int BYTES, int OP>
+__device__ __forceinline__ uint64_t ld_op(const uint8_t *p) {
+    uint64_t a = 0, b = 0, c = 0, d = 0;
+    if constexpr (BYTES == 32) {
+        if constexpr (OP == 0) asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        if constexpr (OP == 1) asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        if constexpr (OP == 2) asm volatile("ld.global.cv.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        if constexpr (OP == 3) asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+        return a ^ b ^ c ^ d;
+    } else {
+        if constexpr (OP == 0) asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        if constexpr (OP == 1) asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        if constexpr (OP == 2) asm volatile("ld.global.cv.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        if constexpr (OP == 3) asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(a) : "l"(p));
+        return a;
+    }
+}
+
+template <int BYTES, int OP>
+__global__ void k_gather_op(const uint8_t *__restrict__ buf, uint64_t slot_mask, uint32_t loads,
+                            uint64_t *__restrict__ sink) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t acc = 0;
+    const uint64_t h = hash64(tid * 0x9E3779B97F4A7C15ull + 0x1234567ull);
+    for (uint32_t i = 0; i < loads; i += 8) {
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_op<BYTES, OP>(buf + (hash64(h + i + u) & slot_mask) * BYTES);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    if (acc == 0x5eed) sink[0] = acc;
+}
+
 // mode 2: random stores of BYTES (partial-sector stores below 32 B exercise the L2 / ECC
 // read-modify-write path of a scattered result write)
 template <int BYTES>
@@ -215,6 +277,12 @@ extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes
         return SA_EINVAL;
     }
     SA_CUDA_TRY(cudaSetDevice(device));
+    // measurement knob of this tool only: SA_L2_FETCH_BYTES=32|64|128 -> cudaLimitMaxL2FetchGranularity
+    if (const char *g = getenv("SA_L2_FETCH_BYTES")) {
+        const int b = atoi(g);
+        if (b == 32 || b == 64 || b == 128) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)b);
+        (void)cudaGetLastError();
+    }
     uint8_t *buf = nullptr;
     uint64_t *sink = nullptr;
     SA_CUDA_TRY(cudaMalloc(&buf, buffer_bytes));
@@ -228,6 +296,17 @@ extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes
     const unsigned threads = 256;
     const unsigned blocks = (unsigned)((n_threads + threads - 1) / threads);
     auto launch = [&]() {
+        if (dependent >= 10 && dependent <= 13 && (access_bytes == 32 || access_bytes == 8)) {
+            const int op = dependent - 10;
+#define SA_GOP(B, O) k_gather_op<B, O><<<blocks, threads>>>(buf, slots - 1, loads, sink)
+            if (access_bytes == 32) {
+                if (op == 0) SA_GOP(32, 0); else if (op == 1) SA_GOP(32, 1); else if (op == 2) SA_GOP(32, 2); else SA_GOP(32, 3);
+            } else {
+                if (op == 0) SA_GOP(8, 0); else if (op == 1) SA_GOP(8, 1); else if (op == 2) SA_GOP(8, 2); else SA_GOP(8, 3);
+            }
+#undef SA_GOP
+            return;
+        }
         if (dependent == 2) {
             switch (access_bytes) {
             case 32: k_scatter<32><<<blocks, threads>>>(buf, slots - 1, loads); break;

@@ -334,38 +334,44 @@ sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out) {
     return SA_OK;
 }
 
-sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) {
+// Upload + validate + pack the reference (chunks of 256 MiB) into idx->text.
+sa_status sa_pack_text(sa_index *idx, const char *ref_ascii, cudaStream_t st) {
     const uint64_t n = idx->n;
-    // ---- 1. upload + validate + pack (chunks of 256 MiB) ----
     idx->n_words = (n + 31) / 32 + kGuardWords;
     SA_CUDA_TRY(cudaMalloc(&idx->text, idx->n_words * sizeof(uint64_t)));
     SA_CUDA_TRY(cudaMemsetAsync(idx->text, 0, idx->n_words * sizeof(uint64_t), st));
-    {
-        const uint64_t CH = 256ull << 20;
-        DevBuf<uint8_t> dbuf;
-        DevBuf<unsigned long long> bad;
-        SA_TRY(dbuf.alloc(n < CH ? n : CH, st, "upload staging"));
-        SA_TRY(bad.alloc(1, st, "validation flag"));
-        SA_CUDA_TRY(cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), st));
-        for (uint64_t off = 0; off < n; off += CH) {
-            const uint64_t len = (n - off < CH) ? n - off : CH;
-            SA_CUDA_TRY(cudaMemcpyAsync(dbuf.p, ref_ascii + off, len, cudaMemcpyHostToDevice, st));
-            k_pack<<<grid_for((len + 31) / 32), kThreads, 0, st>>>(dbuf.p, len, off / 32, idx->text, bad.p);
-            SA_CUDA_TRY(cudaGetLastError());
-        }
-        unsigned long long h_bad = 0;
-        SA_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad.p, sizeof(h_bad), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        if (h_bad != ~0ull) {
-            const unsigned char c = (unsigned char)ref_ascii[h_bad];
-            sa_set_error("reference symbol 0x%02x ('%c') at position %llu is not A/C/G/T", c,
-                         (c >= 32 && c < 127) ? c : '?', h_bad);
-            return SA_ESYMBOL;
-        }
+    const uint64_t CH = 256ull << 20;
+    DevBuf<uint8_t> dbuf;
+    DevBuf<unsigned long long> bad;
+    SA_TRY(dbuf.alloc(n < CH ? n : CH, st, "upload staging"));
+    SA_TRY(bad.alloc(1, st, "validation flag"));
+    SA_CUDA_TRY(cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), st));
+    for (uint64_t off = 0; off < n; off += CH) {
+        const uint64_t len = (n - off < CH) ? n - off : CH;
+        SA_CUDA_TRY(cudaMemcpyAsync(dbuf.p, ref_ascii + off, len, cudaMemcpyHostToDevice, st));
+        k_pack<<<grid_for((len + 31) / 32), kThreads, 0, st>>>(dbuf.p, len, off / 32, idx->text, bad.p);
+        SA_CUDA_TRY(cudaGetLastError());
     }
+    unsigned long long h_bad = 0;
+    SA_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad.p, sizeof(h_bad), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    if (h_bad != ~0ull) {
+        const unsigned char c = (unsigned char)ref_ascii[h_bad];
+        sa_set_error("reference symbol 0x%02x ('%c') at position %llu is not A/C/G/T", c, (c >= 32 && c < 127) ? c : '?',
+                     h_bad);
+        return SA_ESYMBOL;
+    }
+    return SA_OK;
+}
+
+sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) {
+    const uint64_t n = idx->n;
+    // ---- 1. upload + validate + pack ----
+    SA_TRY(sa_pack_text(idx, ref_ascii, st));
     // ---- 2. suffix array ----
     SA_CUDA_TRY(cudaMalloc(&idx->sa, n * sizeof(uint32_t)));
-    SA_TRY(build_sa(idx, st));
+    if (idx->build_dc3) SA_TRY(sa_build_sa_dc3(idx, st, nullptr, nullptr));  // the paper's DC3
+    else SA_TRY(build_sa(idx, st));                                           // prefix doubling (default)
     // ---- 3. k-mer bracket table ----
     const uint64_t K = 1ull << (2 * idx->k);
     SA_CUDA_TRY(cudaMalloc(&idx->table, (K + 1) * sizeof(uint32_t)));

@@ -89,6 +89,7 @@ struct sa_index {
     uint32_t *table = nullptr;   // dev: 4^k + 1 entries
     uint64_t device_bytes = 0;
     uint32_t build_rounds = 0;   // prefix-doubling rounds after the initial sort
+    bool build_dc3 = false;      // SA_INDEX_BUILD_DC3: the SA by DC3 instead of prefix doubling
     // host-buffer pipeline (sa_match_batch_host); grown on demand, guarded by mu
     std::mutex mu;
     cudaStream_t pipe_stream[2] = {nullptr, nullptr};
@@ -162,3 +163,5 @@ inline SaView sa_view(const sa_index *idx) {
 // build / match entry points implemented in sa_build.cu / sa_match.cu
 sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st);
 sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out);
+sa_status sa_pack_text(sa_index *idx, const char *ref_ascii, cudaStream_t st);
+sa_status sa_build_sa_dc3(sa_index *idx, cudaStream_t st, uint32_t *trace_rank, uint32_t *trace_nonsample);
