@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--layout", default="rec32", choices=["rec16", "rec32", "plain"],
                     help="SA layout: 16-byte records caching 48 bases (default), 32-byte records caching 112 "
                          "bases, or a plain uint32 SA")
+    ap.add_argument("--build", default="doubling", choices=["doubling", "dc3"],
+                    help="suffix-array construction (untimed): prefix doubling or the paper's DC3")
     ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
     ap.add_argument("--rows-ordered", action="store_true",
@@ -255,9 +257,10 @@ def main():
     ref = cfg.reference()
     log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
     t0 = time.time()
-    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout)
+    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build)
     torch.cuda.synchronize()
-    log(f"index built in {time.time() - t0:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
+    build_s = time.time() - t0
+    log(f"index built in {build_s:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
     t0 = time.time()
     Q = cfg.Q
     stride = cfg.stride
@@ -340,7 +343,9 @@ def main():
                                           if presort else 0),
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
             "shards": summary_all, "layout": args.layout, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
-            "index_bytes": idx.device_bytes}
+            "index_bytes": idx.device_bytes,
+            "index_build": {"seconds": build_s, "sa_algorithm": args.build,
+                            "note": "untimed: upload + pack + suffix array + k-mer table + records"}}
 
     # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
     chk = torch.empty_like(out)
