@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--build", default="doubling", choices=["doubling", "dc3"],
                     help="suffix-array construction (untimed): prefix doubling or the paper's DC3")
     ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
+    ap.add_argument("--tree", action="store_true",
+                    help="time the flattened suffix tree walk (sa_tree_match, SURVEY.md 8(f) f3) instead of the SA search")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
     ap.add_argument("--rows-ordered", action="store_true",
                     help="the ordering step also gathers the read rows into order (SA_MATCH_ROWS_ORDERED)")
@@ -261,6 +263,11 @@ def main():
     torch.cuda.synchronize()
     build_s = time.time() - t0
     log(f"index built in {build_s:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
+    tree = None
+    if args.tree:
+        t1 = time.time()
+        tree = sa.Tree(idx)
+        log(f"flattened suffix tree: {tree.nodes} nodes, {tree.device_bytes / 1e9:.2f} GB, {time.time() - t1:.1f}s")
     t0 = time.time()
     Q = cfg.Q
     stride = cfg.stride
@@ -293,7 +300,9 @@ def main():
                       ordered_words=owords, ordered_lens=olens)
         if i is not None:
             ev[i][0].record(stream)
-        if rows_ordered:
+        if tree is not None:
+            tree.match(words, lens, fixed_len=fixed, out=out, stream=stream, order=perm)
+        elif rows_ordered:
             idx.match(owords, olens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm, rows_ordered=True)
         else:
             idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm)
@@ -349,6 +358,13 @@ def main():
 
     # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
     chk = torch.empty_like(out)
+    if tree is not None:  # the walk must give the SA search's intervals
+        ref_out = idx.match(words, lens, fixed_len=fixed, stream=stream)
+        torch.cuda.synchronize()
+        if not torch.equal(ref_out, out):
+            raise RuntimeError("suffix-tree walk disagrees with the SA search")
+        line["tree"] = {"nodes": tree.nodes, "bytes": tree.device_bytes, "kernel": "k_tree_match"}
+        del ref_out
     if rows_ordered:
         _, st = idx.match(owords, olens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
                           order=perm, rows_ordered=True)

@@ -182,6 +182,21 @@ sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_
 sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,
                                 uint32_t loads, int32_t dependent, float *ms);
 
+/* Flattened suffix tree ("flatten tree consisting of an
+ * array of edges", Table V STK): built from an index's suffix array (LCP on the GPU, the
+ * lcp-interval tree on the host), 32-byte nodes {lb, rb, string depth, SA[lb], child[a,c,g,t]} in
+ * HBM.  The tree BORROWS the index (destroy the tree first).  Requires n < 2^31.
+ * sa_tree_match walks it from the root, one node and one edge-label compare per branching level,
+ * and writes the same half-open SA intervals as sa_match_batch (out_lohi, 2Q uint32), misses at their
+ * insertion point.  Strided reads only (stride_words >= 1); order as for sa_match_batch (nullable).
+ * Asynchronous on `stream`. */
+typedef struct sa_tree sa_tree;
+sa_status sa_tree_create(const sa_index *idx, sa_tree **out);
+void sa_tree_destroy(sa_tree *tree);
+sa_status sa_tree_info(const sa_tree *tree, uint64_t *nodes, uint64_t *device_bytes);
+sa_status sa_tree_match(const sa_tree *tree, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                        uint32_t stride_words, uint64_t Q, const uint32_t *order, uint32_t *out_lohi, void *stream);
+
 /* DC3 trace for checking the build against the paper's worked example (Tables II-III,
  * P:L112-128): runs DC3 on ref_ascii[0..n) on the current device and returns, on the host,
  * sample_rank[i] = the 1-based rank of S_i among the sample suffixes (i mod 3 != 0; 0 for i mod 3 = 0)

@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 
 import numpy as np
 
-__all__ = ["SAError", "Index", "lib", "random_gather", "LIB_PATH", "EXPORTED_SYMBOLS"]
+__all__ = ["SAError", "Index", "Tree", "lib", "random_gather", "dc3_trace", "LIB_PATH", "EXPORTED_SYMBOLS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SA_LIB_PATH selects another build of the same library (A/B measurements of build variants)
@@ -58,6 +58,10 @@ _SIGS = {
     "sa_locate": ([_p, _p, _p, _u64, _p, _p], ctypes.c_int),
     "sa_tool_random_gather": ([_i32, _u64, _u32, _u64, _u32, _i32, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "sa_dc3_trace": ([_p, _u64, _p, _p], ctypes.c_int),
+    "sa_tree_create": ([_p, ctypes.POINTER(_p)], ctypes.c_int),
+    "sa_tree_destroy": ([_p], None),
+    "sa_tree_info": ([_p, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], ctypes.c_int),
+    "sa_tree_match": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p], ctypes.c_int),
     "sa_last_error": ([], ctypes.c_char_p),
     "sa_version": ([], ctypes.c_int32),
 }
@@ -279,6 +283,39 @@ class Index:
         """Positions SA[lo..hi) of every read (SA order).  Returns (offsets int64 [Q+1], positions int32 [total])."""
         offsets = self.locate_offsets(lohi, stream)
         return offsets, self.locate_positions(lohi, offsets, stream=stream)
+
+
+class Tree:
+    """Flattened suffix tree of an Index (sa_tree_create); keeps the index alive while it lives."""
+
+    def __init__(self, index: "Index"):
+        h = _p()
+        _check(lib().sa_tree_create(index._h, ctypes.byref(h)), "sa_tree_create")
+        self._h, self.index = h, index
+        nodes, nb = _u64(), _u64()
+        _check(lib().sa_tree_info(h, ctypes.byref(nodes), ctypes.byref(nb)), "sa_tree_info")
+        self.nodes, self.device_bytes = nodes.value, nb.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sa_tree_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, order=None):
+        """sa_tree_match: the same [lo, hi) per read as Index.match, by walking the tree."""
+        import torch
+        Q, stride = words.shape
+        if out is None:
+            out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
+        _check(lib().sa_tree_match(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
+                                   _dptr(out), _stream_ptr(stream)), "sa_tree_match")
+        return out
 
 
 def dc3_trace(ref):
