@@ -383,10 +383,14 @@ def main():
     # ---- roofline of the dominant kernel (k_match; the ordering sort is CUB's) ----
     bpq = algorithmic_bytes_per_query(args.layout, m_alg, line["search_stats"]["mean_steps"],
                                       line["search_stats"]["mean_text_windows"])
+    if tree is not None:
+        line["search_stats"]["note"] = "counts of the SA search (the timed kernel is the tree walk)"
     achieved = bpq * Q / avg_launch_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_match", "algorithmic_bytes_per_query": bpq,
-                "peak_source": peak_src}
+                "traffic": traffic, "kernel": "k_tree_match" if tree is not None else "k_match",
+                "algorithmic_bytes_per_query": bpq, "peak_source": peak_src}
+    if tree is not None:
+        roofline["note"] = "bytes model of the SA search; the tree walk moves one 32-B node + one text window per level"
     if traffic:
         roofline["traffic_GBps"] = traffic / avg_launch_s / 1e9
         roofline["traffic_frac"] = roofline["traffic_GBps"] / peak
