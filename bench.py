@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--build", default="doubling", choices=["doubling", "dc3"],
                     help="suffix-array construction (untimed): prefix doubling or the paper's DC3")
     ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
+    ap.add_argument("--chunks", type=int, default=1,
+                    help="split the batch into this many chunks, ordering chunk i+1 on a second stream while "
+                         "chunk i is searched")
     ap.add_argument("--tree", action="store_true",
                     help="time the flattened suffix tree walk (sa_tree_match, SURVEY.md 8(f) f3) instead of the SA search")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
@@ -293,8 +296,30 @@ def main():
     olens = torch.empty_like(lens) if (rows_ordered and lens is not None) else None
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(args.steps)]
 
+    chunks = max(1, args.chunks) if presort and not rows_ordered and tree is None else 1
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(1 if chunks > 1 else 0)]
+    bounds = [Q * c // chunks for c in range(chunks + 1)]
+    ws_c = [ws] + [torch.empty_like(ws) for _ in range(1 if chunks > 1 else 0)]
+    ev_order = [torch.cuda.Event() for _ in range(chunks)]
+
     def step(i=None):
         # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
+        if chunks > 1:
+            # order chunk c on stream c%2 while chunk c-1 is searched on the other; results join at the end
+            if i is not None:
+                ev[i][0].record(stream)
+            streams[1].wait_stream(stream)
+            for c in range(chunks):
+                sc, q0, q1 = streams[c % 2], bounds[c], bounds[c + 1]
+                lw = None if lens is None else lens[q0:q1]
+                idx.order(words[q0:q1], lw, fixed_len=fixed, out=perm[q0:q1], stream=sc, workspace=ws_c[c % 2],
+                          key_bases=args.order_bases)
+                idx.match(words[q0:q1], lw, fixed_len=fixed, out=out[q0:q1], stream=sc, workspace=ws_c[c % 2],
+                          order=perm[q0:q1])
+            stream.wait_stream(streams[1])
+            if i is not None:
+                ev[i][1].record(stream)  # chunked: the "launch" time is the whole overlapped step
+            return
         if presort:
             idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws, key_bases=args.order_bases,
                       ordered_words=owords, ordered_lens=olens)
