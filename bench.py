@@ -393,9 +393,9 @@ def main():
     if rows_ordered:
         _, st = idx.match(owords, olens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
                           order=perm, rows_ordered=True)
-    else:
+    else:  # (with --chunks the permutation is chunk-local: any order gives the same intervals)
         _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
-                          order=perm)
+                          order=perm if chunks == 1 else None)
     torch.cuda.synchronize()
     if not torch.equal(chk, out):
         raise RuntimeError("instrumented launch disagrees with the timed launches")
