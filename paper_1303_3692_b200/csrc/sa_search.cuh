@@ -380,4 +380,41 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
 }
 
+// Software-pipelined variant: each thread takes R read slots (t, t+G, t+2G, ... with G the grid
+// size) and issues the loads of the next read's order entry and row before searching the current
+// read, so the head of each read's dependent chain (order -> row) overlaps the previous search.
+template <int QW, int L, bool STATS>
+__global__ void __launch_bounds__(256) k_match_pipe(const MatchArgs a) {
+    const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.Q) return;
+    uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
+    uint64_t row = a.rows_ordered ? t : q;
+    uint32_t m = read_len(a, row);
+    QueryWords<QW> P;
+    load_read<QW>(a, row, m, P);
+    for (;;) {
+        const uint64_t tn = t + G;
+        const bool more = tn < a.Q;
+        uint64_t qn = 0, rown = 0;
+        uint32_t mn = 0;
+        QueryWords<QW> Pn;
+        if (more) {  // prefetch the next read (independent of the search below)
+            qn = a.order ? (uint64_t)__ldg(a.order + tn) : tn;
+            rown = a.rows_ordered ? tn : qn;
+            mn = read_len(a, rown);
+            load_read<QW>(a, rown, mn, Pn);
+        }
+        uint32_t lo, hi, steps = 0, texts = 0;
+        search_read<QW, L>(a, P, m, lo, hi, steps, texts);
+        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+        if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+        if (!more) break;
+        t = tn;
+        q = qn;
+        m = mn;
+        P = Pn;
+    }
+}
+
 }  // namespace sa_search
