@@ -24,13 +24,10 @@ $(PKG)/libsa.so: $(CU_SRCS) $(CU_HDRS)
 $(shell mkdir -p build)
 
 # A/B build variants (variants/*.so; bench.py / tests load one with SA_LIB_PATH=...)
-VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ldca.so variants/libsa_pipe2.so variants/libsa_pipe4.so variants/libsa_pipe8.so
+VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ldca.so
 variants/libsa_ldcg.so: DEFS := -DSA_LD_MODE=1
 variants/libsa_ldnoalloc.so: DEFS := -DSA_LD_MODE=2
 variants/libsa_ldca.so: DEFS := -DSA_LD_MODE=3
-variants/libsa_pipe2.so: DEFS := -DSA_PIPE_READS=2
-variants/libsa_pipe4.so: DEFS := -DSA_PIPE_READS=4
-variants/libsa_pipe8.so: DEFS := -DSA_PIPE_READS=8
 variants: $(VARIANTS)
 variants/%.so: $(CU_SRCS) $(CU_HDRS)
 	mkdir -p variants && $(NVCC) $(NVFLAGS) $(DEFS) -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_$(notdir $@).log || (cat build/ptxas_$(notdir $@).log; false)

@@ -15,20 +15,9 @@ namespace {
 
 using sa_search::MatchArgs;
 
-// SA_PIPE_READS (compile-time A/B): reads per thread of the software-pipelined kernel (0 = off)
-#ifndef SA_PIPE_READS
-#define SA_PIPE_READS 0
-#endif
-
 template <int QW, int L, bool STATS>
 cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     const int threads = 256;
-    if (SA_PIPE_READS > 1) {
-        const uint64_t per = (uint64_t)threads * SA_PIPE_READS;
-        const unsigned blocks = (unsigned)((a.Q + per - 1) / per);
-        sa_search::k_match_pipe<QW, L, STATS><<<blocks, threads, 0, st>>>(a);
-        return cudaGetLastError();
-    }
     const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
     sa_search::k_match<QW, L, STATS><<<blocks, threads, 0, st>>>(a);
     return cudaGetLastError();

@@ -361,9 +361,11 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 }
 
 // One read per thread slot, all lanes of a warp in lock step (with sa_match_order the lanes hold
-// lexicographically adjacent reads and walk neighbouring parts of the SA and table).  A persistent,
-// lane-refilling variant (a finished lane takes the next read) was measured slower on B200 at C4
-// (profiles/r01b, r01c: it de-correlates the lanes' addresses and scatters loads and stores).
+// lexicographically adjacent reads and walk neighbouring parts of the SA and table).  Measured and
+// dropped on B200 at C4: a persistent lane-refilling variant (a finished lane takes the next read;
+// profiles/r01b, r01c: it de-correlates the lanes' addresses), and a software-pipelined variant that
+// prefetches the next read's row during the current search (profiles/r01t: 2% slower -- the kernel is
+// bound by DRAM line throughput, not by the latency of the chain's head).
 template <int QW, int L, bool STATS>
 __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -378,43 +380,6 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
     reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
-}
-
-// Software-pipelined variant: each thread takes R read slots (t, t+G, t+2G, ... with G the grid
-// size) and issues the loads of the next read's order entry and row before searching the current
-// read, so the head of each read's dependent chain (order -> row) overlaps the previous search.
-template <int QW, int L, bool STATS>
-__global__ void __launch_bounds__(256) k_match_pipe(const MatchArgs a) {
-    const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.Q) return;
-    uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
-    uint64_t row = a.rows_ordered ? t : q;
-    uint32_t m = read_len(a, row);
-    QueryWords<QW> P;
-    load_read<QW>(a, row, m, P);
-    for (;;) {
-        const uint64_t tn = t + G;
-        const bool more = tn < a.Q;
-        uint64_t qn = 0, rown = 0;
-        uint32_t mn = 0;
-        QueryWords<QW> Pn;
-        if (more) {  // prefetch the next read (independent of the search below)
-            qn = a.order ? (uint64_t)__ldg(a.order + tn) : tn;
-            rown = a.rows_ordered ? tn : qn;
-            mn = read_len(a, rown);
-            load_read<QW>(a, rown, mn, Pn);
-        }
-        uint32_t lo, hi, steps = 0, texts = 0;
-        search_read<QW, L>(a, P, m, lo, hi, steps, texts);
-        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
-        if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
-        if (!more) break;
-        t = tn;
-        q = qn;
-        m = mn;
-        P = Pn;
-    }
 }
 
 }  // namespace sa_search
