@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-locate", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo only to test the multi-rank path with ranks sharing a GPU)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -251,9 +253,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+    ndev = torch.cuda.device_count()
+    if local >= ndev:  # test mode only (--dist-backend gloo): several ranks share the visible GPUs
+        if args.dist_backend == "nccl":
+            raise RuntimeError(f"LOCAL_RANK {local} but only {ndev} GPUs visible")
+        local = local % ndev
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     cfg = workload(args)
 

@@ -31,6 +31,8 @@ def max_over_ranks(value: float, device) -> float:
     """Max of a per-rank scalar (elapsed ms) over the default group; identity when not distributed."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
+    if dist.get_backend() != "nccl":
+        device = "cpu"  # gloo reduces host tensors
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -40,6 +42,8 @@ def gather_summaries(summary: torch.Tensor) -> List[List[int]]:
     """All ranks' summaries, in rank order."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return [summary.cpu().tolist()]
+    if dist.get_backend() != "nccl":
+        summary = summary.cpu()
     parts = [torch.empty_like(summary) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, summary)
     return [p.cpu().tolist() for p in parts]
