@@ -338,7 +338,7 @@ def test_c4_full_size():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("m", [16, 150, 1000])
+@pytest.mark.parametrize("m", [16, 32, 64, 150, 250, 500, 1000])
 def test_c5_read_lengths_full_reference(m):
     # C5's reference (= C4's) at a sample of its read lengths; 2M reads per length
     _full_size_check(synth.CONFIGS["C5"].with_m(m), sample=128, q_count=2_000_000)
