@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--chunks", type=int, default=1,
                     help="split the batch into this many chunks, ordering chunk i+1 on a second stream while "
                          "chunk i is searched")
+    ap.add_argument("--partition", action="store_true",
+                    help="SURVEY.md 8(f) f4: each rank holds 1/WORLD_SIZE of the index (route-key range) and reads "
+                         "are exchanged with all-to-alls (shard.partitioned_match)")
     ap.add_argument("--tree", action="store_true",
                     help="time the flattened suffix tree walk (sa_tree_match, SURVEY.md 8(f) f3) instead of the SA search")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
@@ -272,7 +275,8 @@ def main():
     ref = cfg.reference()
     log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
     t0 = time.time()
-    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build)
+    part = (rank, world, 12) if args.partition else None
+    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build, part=part)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     log(f"index built in {build_s:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
@@ -314,6 +318,13 @@ def main():
 
     def step(i=None):
         # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
+        if args.partition:
+            if i is not None:
+                ev[i][0].record(stream)
+            shard.partitioned_match(idx, words, lens, fixed_len=fixed, out=out)
+            if i is not None:
+                ev[i][1].record(stream)
+            return
         if chunks > 1:
             # order chunk c on stream c%2 while chunk c-1 is searched on the other; results join at the end
             if i is not None:
@@ -391,50 +402,55 @@ def main():
             "index_build": {"seconds": build_s, "sa_algorithm": args.build,
                             "note": "untimed: upload + pack + suffix array + k-mer table + records"}}
 
-    # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
-    chk = torch.empty_like(out)
-    if tree is not None:  # the walk must give the SA search's intervals
-        ref_out = idx.match(words, lens, fixed_len=fixed, stream=stream)
+    if not args.partition:
+        # ---- search statistics (untimed instrumented launch): steps and text windows per read ----
+        chk = torch.empty_like(out)
+        if tree is not None:  # the walk must give the SA search's intervals
+            ref_out = idx.match(words, lens, fixed_len=fixed, stream=stream)
+            torch.cuda.synchronize()
+            if not torch.equal(ref_out, out):
+                raise RuntimeError("suffix-tree walk disagrees with the SA search")
+            line["tree"] = {"nodes": tree.nodes, "bytes": tree.device_bytes, "kernel": "k_tree_match"}
+            del ref_out
+        if rows_ordered:
+            _, st = idx.match(owords, olens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
+                              order=perm, rows_ordered=True)
+        else:  # (with --chunks the permutation is chunk-local: any order gives the same intervals)
+            _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
+                              order=perm if chunks == 1 else None)
         torch.cuda.synchronize()
-        if not torch.equal(ref_out, out):
-            raise RuntimeError("suffix-tree walk disagrees with the SA search")
-        line["tree"] = {"nodes": tree.nodes, "bytes": tree.device_bytes, "kernel": "k_tree_match"}
-        del ref_out
-    if rows_ordered:
-        _, st = idx.match(owords, olens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
-                          order=perm, rows_ordered=True)
-    else:  # (with --chunks the permutation is chunk-local: any order gives the same intervals)
-        _, st = idx.match(words, lens, fixed_len=fixed, out=chk, stream=stream, want_stats=True, workspace=ws,
-                          order=perm if chunks == 1 else None)
-    torch.cuda.synchronize()
-    if not torch.equal(chk, out):
-        raise RuntimeError("instrumented launch disagrees with the timed launches")
-    stv = st.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    steps_t, texts_t = (stv & 0xFFFF).double(), (stv >> 16).double()
-    line["search_stats"] = {"mean_steps": float(steps_t.mean()), "mean_text_windows": float(texts_t.mean()),
-                            "p99_steps": float(torch.quantile(steps_t[:1 << 20], 0.99)),
-                            "max_steps": float(steps_t.max())}
+        if not torch.equal(chk, out):
+            raise RuntimeError("instrumented launch disagrees with the timed launches")
+        stv = st.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        steps_t, texts_t = (stv & 0xFFFF).double(), (stv >> 16).double()
+        line["search_stats"] = {"mean_steps": float(steps_t.mean()), "mean_text_windows": float(texts_t.mean()),
+                                "p99_steps": float(torch.quantile(steps_t[:1 << 20], 0.99)),
+                                "max_steps": float(steps_t.max())}
 
-    # ---- roofline of the dominant kernel (k_match; the ordering sort is CUB's) ----
-    bpq = algorithmic_bytes_per_query(args.layout, m_alg, line["search_stats"]["mean_steps"],
-                                      line["search_stats"]["mean_text_windows"])
-    if tree is not None:
-        line["search_stats"]["note"] = "counts of the SA search (the timed kernel is the tree walk)"
-    achieved = bpq * Q / avg_launch_s / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "k_tree_match" if tree is not None else "k_match",
-                "algorithmic_bytes_per_query": bpq, "peak_source": peak_src}
-    if tree is not None:
-        roofline["note"] = "bytes model of the SA search; the tree walk moves one 32-B node + one text window per level"
-    if traffic:
-        roofline["traffic_GBps"] = traffic / avg_launch_s / 1e9
-        roofline["traffic_frac"] = roofline["traffic_GBps"] / peak
-    line["roofline"] = roofline
-    del st, chk
+        # ---- roofline of the dominant kernel (k_match; the ordering sort is CUB's) ----
+        bpq = algorithmic_bytes_per_query(args.layout, m_alg, line["search_stats"]["mean_steps"],
+                                          line["search_stats"]["mean_text_windows"])
+        if tree is not None:
+            line["search_stats"]["note"] = "counts of the SA search (the timed kernel is the tree walk)"
+        achieved = bpq * Q / avg_launch_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "kernel": "k_tree_match" if tree is not None else "k_match",
+                    "algorithmic_bytes_per_query": bpq, "peak_source": peak_src}
+        if tree is not None:
+            roofline["note"] = "bytes model of the SA search; the tree walk moves one 32-B node + one text window per level"
+        if traffic:
+            roofline["traffic_GBps"] = traffic / avg_launch_s / 1e9
+            roofline["traffic_frac"] = roofline["traffic_GBps"] / peak
+        line["roofline"] = roofline
+        del st, chk
 
     # ---- locate (separate call): positions SA[lo..hi) of the reads ----
     # Repeat-rich references give some reads 10^5+ occurrences, so the located prefix of the batch is
     # capped at 2^30 positions (4 GiB); the line says how many reads and positions were located.
+    if args.partition:  # the batch was answered across ranks: no per-rank stats / locate / e2e
+        args.no_locate = args.no_e2e = True
+        line["partition"] = idx.part_info()
+        line["partition"].pop("part_keys")
     if not args.no_locate:
         torch.cuda.synchronize()
         l0, l1, l2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))

@@ -182,6 +182,30 @@ sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_
 sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,
                                 uint32_t loads, int32_t dependent, float *ms);
 
+/* Partitioned index: for references whose index exceeds one GPU, rank
+ * `part` of `nparts` keeps only the reads' route range [part_keys[part], part_keys[part+1]) of the
+ * first route_bases bases (route_bases < k): the SA ranks and bracket-table entries those reads can
+ * touch, plus the whole packed text.  Boundaries balance the SA ranks over the parts.  (This version
+ * builds the whole index on each rank first and then keeps its slice.)  A partition answers reads of
+ * length >= k only (shorter ones get lo = hi = 0xFFFFFFFF); its intervals are global SA ranks.
+ *   sa_index_part_info: part_keys receives nparts+1 route-key boundaries.
+ *   sa_match_route:     orders a batch by route key (order, as sa_match_order), gathers the rows in that
+ *                       order (ordered_words/_len, as SA_MATCH_ROWS_ORDERED) and writes dest_offsets
+ *                       (dev, nparts+1 uint64): the reads for part g are ordered rows
+ *                       [dest_offsets[g], dest_offsets[g+1]).  Workspace: sa_match_order_workspace_size.
+ *   sa_scatter_results: out_lohi[order[t]] = in_lohi[t] (results back in the batch's own order).
+ * The exchange itself (an all-to-all of rows and of intervals) is the caller's collective
+ * (paper_1303_3692_b200/shard.py: torch.distributed all_to_all_single over NCCL). */
+sa_status sa_index_create_part(const char *ref_ascii, uint64_t n, const sa_index_opts *opts, uint32_t part,
+                               uint32_t nparts, uint32_t route_bases, sa_index **out);
+sa_status sa_index_part_info(const sa_index *idx, uint32_t *part, uint32_t *nparts, uint32_t *route_bases,
+                             uint64_t *rank_lo, uint64_t *rank_hi, uint32_t *part_keys);
+sa_status sa_match_route(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
+                         uint32_t stride_words, uint64_t Q, uint32_t *order, uint64_t *ordered_words,
+                         uint32_t *ordered_len, uint64_t *dest_offsets, void *workspace, size_t ws_bytes, void *stream);
+sa_status sa_scatter_results(const uint32_t *order, const uint32_t *in_lohi, uint64_t Q, uint32_t *out_lohi,
+                             void *stream);
+
 /* Flattened suffix tree ("flatten tree consisting of an
  * array of edges", Table V STK): built from an index's suffix array (LCP on the GPU, the
  * lcp-interval tree on the host), 32-byte nodes {lb, rb, string depth, SA[lb], child[a,c,g,t]} in

@@ -58,6 +58,11 @@ _SIGS = {
     "sa_locate": ([_p, _p, _p, _u64, _p, _p], ctypes.c_int),
     "sa_tool_random_gather": ([_i32, _u64, _u32, _u64, _u32, _i32, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "sa_dc3_trace": ([_p, _u64, _p, _p], ctypes.c_int),
+    "sa_index_create_part": ([_p, _u64, ctypes.POINTER(_Opts), _u32, _u32, _u32, ctypes.POINTER(_p)], ctypes.c_int),
+    "sa_index_part_info": ([_p, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32),
+                            ctypes.POINTER(_u64), ctypes.POINTER(_u64), _p], ctypes.c_int),
+    "sa_match_route": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
+    "sa_scatter_results": ([_p, _p, _u64, _p, _p], ctypes.c_int),
     "sa_tree_create": ([_p, ctypes.POINTER(_p)], ctypes.c_int),
     "sa_tree_destroy": ([_p], None),
     "sa_tree_info": ([_p, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], ctypes.c_int),
@@ -127,7 +132,8 @@ class Index:
     build: "doubling" (default, prefix doubling) or "dc3" (the paper's DC3, SA_INDEX_BUILD_DC3).
     """
 
-    def __init__(self, ref, k: int = 0, device: Optional[int] = None, layout: str = "rec16", build: str = "doubling"):
+    def __init__(self, ref, k: int = 0, device: Optional[int] = None, layout: str = "rec16", build: str = "doubling",
+                 part: Optional[Tuple[int, int, int]] = None):
         if isinstance(ref, str):
             ref = ref.encode("ascii")
         arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
@@ -138,13 +144,43 @@ class Index:
         opts = _Opts(-1 if device is None else int(device), int(k), flags, 0)
         self.layout = layout
         h = _p()
-        _check(lib().sa_index_create(arr.ctypes.data if arr.size else None, arr.size, ctypes.byref(opts),
-                                     ctypes.byref(h)), "sa_index_create")
+        ptr = arr.ctypes.data if arr.size else None
+        if part is None:
+            _check(lib().sa_index_create(ptr, arr.size, ctypes.byref(opts), ctypes.byref(h)), "sa_index_create")
+        else:  # (part, nparts, route_bases): a partition of the index
+            _check(lib().sa_index_create_part(ptr, arr.size, ctypes.byref(opts), int(part[0]), int(part[1]),
+                                              int(part[2]), ctypes.byref(h)), "sa_index_create_part")
         self._h = h
         n, kk, nb, dev = _u64(), _u32(), _u64(), _i32()
         _check(lib().sa_index_info(h, ctypes.byref(n), ctypes.byref(kk), ctypes.byref(nb), ctypes.byref(dev)),
                "sa_index_info")
         self.n, self.k, self.device_bytes, self.device = n.value, kk.value, nb.value, dev.value
+
+    def part_info(self) -> dict:
+        p, np_, rb, lo, hi = _u32(), _u32(), _u32(), _u64(), _u64()
+        _check(lib().sa_index_part_info(self._h, ctypes.byref(p), ctypes.byref(np_), ctypes.byref(rb),
+                                        ctypes.byref(lo), ctypes.byref(hi), None), "sa_index_part_info")
+        keys = np.empty(np_.value + 1, dtype=np.uint32)
+        _check(lib().sa_index_part_info(self._h, None, None, None, None, None, keys.ctypes.data), "sa_index_part_info")
+        return {"part": p.value, "nparts": np_.value, "route_bases": rb.value, "rank_lo": lo.value,
+                "rank_hi": hi.value, "part_keys": keys.tolist()}
+
+    def route(self, words, lens=None, fixed_len: Optional[int] = None, stream=None):
+        """sa_match_route: (order int32[Q], ordered words, ordered lens or None, dest offsets int64[nparts+1])."""
+        import torch
+        Q, stride = words.shape
+        need = _sz()
+        _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(need)), "sa_match_order_workspace_size")
+        ws = torch.empty(max(1, need.value), dtype=torch.uint8, device=words.device)
+        order = torch.empty(Q, dtype=torch.int32, device=words.device)
+        ow = torch.empty_like(words)
+        ol = None if lens is None else torch.empty_like(lens)
+        nparts = self.part_info()["nparts"]
+        offs = torch.empty(nparts + 1, dtype=torch.int64, device=words.device)
+        _check(lib().sa_match_route(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
+                                    _dptr(ow), _dptr(ol), _dptr(offs), _dptr(ws), need.value, _stream_ptr(stream)),
+               "sa_match_route")
+        return order, ow, ol, offs
 
     # ---- lifetime ----
     def close(self):
@@ -316,6 +352,17 @@ class Tree:
         _check(lib().sa_tree_match(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
                                    _dptr(out), _stream_ptr(stream)), "sa_tree_match")
         return out
+
+
+def scatter_results(order, in_lohi, out=None, stream=None):
+    """sa_scatter_results: out[order[t]] = in_lohi[t]."""
+    import torch
+    Q = in_lohi.shape[0]
+    if out is None:
+        out = torch.empty_like(in_lohi)
+    _check(lib().sa_scatter_results(_dptr(order), _dptr(in_lohi), Q, _dptr(out), _stream_ptr(stream)),
+           "sa_scatter_results")
+    return out
 
 
 def dc3_trace(ref):

@@ -108,6 +108,102 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
 
 extern "C" void sa_index_destroy(sa_index *idx) { free_index(idx); }
 
+// ---- partitioned index -----------------------------------------------
+static uint32_t table_at(const sa_index *idx, uint64_t x) {
+    uint32_t v = 0;
+    cudaMemcpy(&v, idx->table + x, 4, cudaMemcpyDeviceToHost);
+    return v;
+}
+
+extern "C" sa_status sa_index_create_part(const char *ref_ascii, uint64_t n, const sa_index_opts *opts, uint32_t part,
+                                          uint32_t nparts, uint32_t route_bases, sa_index **out) {
+    sa_clear_error();
+    if (!out) { sa_set_error("out is NULL"); return SA_EINVAL; }
+    *out = nullptr;
+    if (nparts == 0 || part >= nparts || route_bases == 0 || route_bases > 16) {
+        sa_set_error("bad partition %u of %u / route_bases %u", part, nparts, route_bases);
+        return SA_EINVAL;
+    }
+    sa_index *idx = nullptr;
+    SA_TRY(sa_index_create(ref_ascii, n, opts, &idx));  // the whole index, then keep this rank's slice
+    if (route_bases >= idx->k) {  // slices then start on 4-entry table boundaries
+        sa_index_destroy(idx);
+        sa_set_error("route_bases %u must be < k %u", route_bases, idx->k);
+        return SA_EINVAL;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(idx->device);
+    const uint32_t sh = 2 * (idx->k - route_bases);
+    const uint64_t nkeys = 1ull << (2 * route_bases);
+    // boundaries: part_keys[g] = the smallest route key whose first suffix has rank >= g*n/nparts
+    std::vector<uint32_t> keys(nparts + 1);
+    keys[0] = 0;
+    keys[nparts] = (uint32_t)nkeys;
+    for (uint32_t g = 1; g < nparts; ++g) {
+        const uint64_t target = (uint64_t)g * n / nparts;
+        uint64_t lo = keys[g - 1], hi = nkeys;  // first key K in [lo, nkeys] with T[K << sh] >= target
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (table_at(idx, mid << sh) >= target) hi = mid; else lo = mid + 1;
+        }
+        keys[g] = (uint32_t)lo;
+    }
+    const uint64_t x0 = (uint64_t)keys[part] << sh, x1 = (uint64_t)keys[part + 1] << sh;  // table [x0, x1]
+    const uint64_t r0 = table_at(idx, x0), r1 = table_at(idx, x1);                         // ranks [r0, r1)
+    // slice the table and the SA
+    uint32_t *tab = nullptr;
+    void *sa_slice = nullptr;
+    const uint64_t per = idx->layout == 0 ? 4 : (idx->layout == 2 ? 32 : 16);  // bytes per SA entry
+    cudaError_t e = cudaMalloc(&tab, (x1 - x0 + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(tab, idx->table + x0, (x1 - x0 + 1) * 4, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&sa_slice, (r1 - r0 ? r1 - r0 : 1) * per);
+    const void *src = idx->layout == 0 ? (const void *)(idx->sa + r0) : (const void *)((const uint8_t *)idx->rec + r0 * per);
+    if (e == cudaSuccess && r1 > r0) e = cudaMemcpy(sa_slice, src, (r1 - r0) * per, cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        cudaFree(tab);
+        cudaFree(sa_slice);
+        sa_index_destroy(idx);
+        cudaSetDevice(prev);
+        sa_set_error("partition slice: %s", cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SA_ENOMEM : SA_ECUDA;
+    }
+    cudaFree(idx->table);
+    cudaFree(idx->sa);
+    cudaFree(idx->rec);
+    idx->table = tab;
+    idx->sa = idx->layout == 0 ? (uint32_t *)sa_slice : nullptr;
+    idx->rec = idx->layout == 0 ? nullptr : (uint4 *)sa_slice;
+    idx->part = part;
+    idx->nparts = nparts;
+    idx->route_bases = route_bases;
+    idx->x_base = x0;
+    idx->rank_base = r0;
+    idx->rank_end = r1;
+    idx->part_keys = keys;
+    idx->device_bytes = idx->n_words * 8 + (x1 - x0 + 1) * 4 + (r1 - r0) * per;
+    cudaSetDevice(prev);
+    *out = idx;
+    return SA_OK;
+}
+
+extern "C" sa_status sa_index_part_info(const sa_index *idx, uint32_t *part, uint32_t *nparts, uint32_t *route_bases,
+                                        uint64_t *rank_lo, uint64_t *rank_hi, uint32_t *part_keys) {
+    sa_clear_error();
+    if (!idx) { sa_set_error("index is NULL"); return SA_EINVAL; }
+    if (part) *part = idx->part;
+    if (nparts) *nparts = idx->nparts;
+    if (route_bases) *route_bases = idx->route_bases;
+    if (rank_lo) *rank_lo = idx->rank_base;
+    if (rank_hi) *rank_hi = idx->nparts > 1 ? idx->rank_end : idx->n;
+    if (part_keys) {
+        if (idx->nparts > 1) for (uint32_t g = 0; g <= idx->nparts; ++g) part_keys[g] = idx->part_keys[g];
+        else { part_keys[0] = 0; part_keys[1] = 0xFFFFFFFFu; }
+    }
+    return SA_OK;
+}
+
 extern "C" sa_status sa_dc3_trace(const char *ref_ascii, uint64_t n, uint32_t *sample_rank, uint32_t *nonsample) {
     sa_clear_error();
     if (!ref_ascii || n == 0) { sa_set_error("empty or NULL reference"); return SA_EINVAL; }
@@ -153,12 +249,14 @@ static sa_status export_copy(const sa_index *idx, void *dst, const void *src, si
 extern "C" sa_status sa_index_export_sa(const sa_index *idx, uint32_t *host_out) {
     sa_clear_error();
     if (!idx || !host_out) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    if (idx->nparts > 1) { sa_set_error("a partition holds only a slice of the SA"); return SA_EINVAL; }
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     return sa_extract_sa(idx, host_out);
 }
 
 extern "C" sa_status sa_index_export_table(const sa_index *idx, uint32_t *host_out) {
     sa_clear_error();
+    if (idx && idx->nparts > 1) { sa_set_error("a partition holds only a slice of the table"); return SA_EINVAL; }
     return export_copy(idx, host_out, idx ? idx->table : nullptr,
                        idx ? ((1ull << (2 * idx->k)) + 1) * sizeof(uint32_t) : 0);
 }

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
+#include <vector>
 
 #include "sa.h"
 
@@ -90,6 +91,12 @@ struct sa_index {
     uint64_t device_bytes = 0;
     uint32_t build_rounds = 0;   // prefix-doubling rounds after the initial sort
     bool build_dc3 = false;      // SA_INDEX_BUILD_DC3: the SA by DC3 instead of prefix doubling
+    // partitioned index (sa_index_create_part): this index holds SA ranks [rank_base, rank_end) and
+    // table entries [x_base, x_end] only, i.e. the reads whose first route_bases bases lie in
+    // [part_keys[part], part_keys[part+1])
+    uint32_t part = 0, nparts = 1, route_bases = 0;
+    uint64_t x_base = 0, rank_base = 0, rank_end = 0;
+    std::vector<uint32_t> part_keys;
     // host-buffer pipeline (sa_match_batch_host); grown on demand, guarded by mu
     std::mutex mu;
     cudaStream_t pipe_stream[2] = {nullptr, nullptr};
@@ -155,9 +162,11 @@ __device__ __forceinline__ uint64_t prefix_mask(unsigned L) {
     return L >= 32 ? ~0ull : (L == 0 ? 0ull : ~(~0ull >> (2u * L)));
 }
 
+// (for a partition the base is shifted so that global SA ranks index it)
 inline SaView sa_view(const sa_index *idx) {
-    if (idx->layout == 0) return SaView{idx->sa, 1u};
-    return SaView{reinterpret_cast<const uint32_t *>(idx->rec), idx->layout == 2 ? 8u : 4u};
+    if (idx->layout == 0) return SaView{idx->sa - idx->rank_base, 1u};
+    const uint32_t stride = idx->layout == 2 ? 8u : 4u;
+    return SaView{reinterpret_cast<const uint32_t *>(idx->rec) - idx->rank_base * stride, stride};
 }
 
 // build / match entry points implemented in sa_build.cu / sa_match.cu

@@ -125,6 +125,27 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     return SA_OK;
 }
 
+// ---- partitioned matching ----------------------------------------------
+// offsets[g] = first slot of the sorted keys with key >= part_keys[g] (lower bound)
+__global__ void k_route_offsets(const uint32_t *__restrict__ sorted_keys, uint64_t Q, const uint32_t *__restrict__ bounds,
+                                uint32_t nb, uint64_t *__restrict__ offsets) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nb) return;
+    const uint64_t key = bounds[g];
+    uint64_t lo = 0, hi = Q;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if ((uint64_t)sorted_keys[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    offsets[g] = lo;
+}
+
+__global__ void k_scatter_results(const uint32_t *__restrict__ order, const uint2 *__restrict__ in, uint64_t Q,
+                                  uint2 *__restrict__ out) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (uint64_t)gridDim.x * blockDim.x)
+        out[__ldg(order + t)] = in[t];
+}
+
 // ---- locate -----------------------------------------------------------------------------------
 struct CountOp {
     const uint32_t *lohi;
@@ -244,6 +265,15 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.out = out;
     a.stats = stats;
     a.order = order;
+    a.min_len = 0;
+    if (idx->nparts > 1) {
+        // a partition holds table entries [x_base, x_end] and SA ranks [rank_base, rank_end): address them
+        // with their global indices through shifted base pointers (only in-slice indices are dereferenced)
+        a.table = idx->table - idx->x_base;
+        if (idx->layout == 0) a.sa = idx->sa - idx->rank_base;
+        else a.rec = idx->rec - idx->rank_base * (idx->layout == 2 ? 2 : 1);
+        a.min_len = idx->k;
+    }
     // one vector load per read row when the row is exactly QW words and suitably aligned
     const uintptr_t wp = reinterpret_cast<uintptr_t>(q_words);
     a.vec_rows = (stride == 4 && (wp & 31) == 0) || (stride == 2 && (wp & 15) == 0);
@@ -349,6 +379,62 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
     }
     SA_CUDA_TRY(cudaStreamSynchronize(idx->pipe_stream[0]));
     SA_CUDA_TRY(cudaStreamSynchronize(idx->pipe_stream[1]));
+    return SA_OK;
+}
+
+extern "C" sa_status sa_match_route(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
+                                    uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t *order,
+                                    uint64_t *ordered_words, uint32_t *ordered_len, uint64_t *dest_offsets,
+                                    void *workspace, size_t ws_bytes, void *stream) {
+    sa_clear_error();
+    SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, order));
+    if (!dest_offsets || !ordered_words || stride_words == 0) {
+        sa_set_error("sa_match_route needs dest_offsets, ordered_words and strided reads");
+        return SA_EINVAL;
+    }
+    if (idx->nparts < 2) { sa_set_error("not a partitioned index"); return SA_EINVAL; }
+    SA_CUDA_TRY(cudaSetDevice(idx->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t nb = idx->nparts + 1;
+    if (Q == 0) {
+        SA_CUDA_TRY(cudaMemsetAsync(dest_offsets, 0, nb * sizeof(uint64_t), st));
+        return SA_OK;
+    }
+    PresortLayout L;
+    SA_TRY(presort_layout(Q, false, true, true, L));
+    if (!workspace || ws_bytes < L.total) {
+        sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+        return SA_EINVAL;
+    }
+    uint8_t *ws = static_cast<uint8_t *>(workspace);
+    SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, idx->route_bases, ws, L, order, st));
+    uint64_t blocks = (Q + 255) / 256;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    const bool vec = stride_words == 4 && (reinterpret_cast<uintptr_t>(q_words) & 31) == 0 &&
+                     (reinterpret_cast<uintptr_t>(ordered_words) & 31) == 0;
+    k_gather_rows<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, vec ? 4u : stride_words, Q, order, ordered_words,
+                                                   ordered_len);
+    SA_CUDA_TRY(cudaGetLastError());
+    DevBuf<uint32_t> bounds;
+    SA_TRY(bounds.alloc(nb, st, "route bounds"));
+    SA_CUDA_TRY(cudaMemcpyAsync(bounds.p, idx->part_keys.data(), nb * 4, cudaMemcpyHostToDevice, st));
+    k_route_offsets<<<(nb + 63) / 64, 64, 0, st>>>(reinterpret_cast<const uint32_t *>(ws + L.keys_out), Q, bounds.p, nb,
+                                                   dest_offsets);
+    SA_CUDA_TRY(cudaGetLastError());
+    SA_CUDA_TRY(cudaStreamSynchronize(st));  // bounds is freed on return; keep the copy stream-ordered
+    return SA_OK;
+}
+
+extern "C" sa_status sa_scatter_results(const uint32_t *order, const uint32_t *in_lohi, uint64_t Q, uint32_t *out_lohi,
+                                        void *stream) {
+    sa_clear_error();
+    if (Q == 0) return SA_OK;
+    if (!order || !in_lohi || !out_lohi) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    uint64_t blocks = (Q + 255) / 256;
+    if (blocks > 148ull * 32) blocks = 148ull * 32;
+    k_scatter_results<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        order, reinterpret_cast<const uint2 *>(in_lohi), Q, reinterpret_cast<uint2 *>(out_lohi));
+    SA_CUDA_TRY(cudaGetLastError());
     return SA_OK;
 }
 

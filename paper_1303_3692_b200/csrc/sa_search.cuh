@@ -40,6 +40,7 @@ struct MatchArgs {
     bool vec_rows;                      // read rows can be loaded with one vector load (aligned, stride == QW)
     uint64_t dense_words;               // stride == 0: dense layout, words = one 2-bit stream of this many words
     bool rows_ordered;                  // SA_MATCH_ROWS_ORDERED: row t is read order[t]
+    uint32_t min_len;                   // partitioned index: reads shorter than k get (~0, ~0)
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -376,7 +377,11 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     QueryWords<QW> P;
     load_read<QW>(a, row, m, P);
     uint32_t lo, hi, steps = 0, texts = 0;
-    search_read<QW, L>(a, P, m, lo, hi, steps, texts);
+    if (m < a.min_len) {  // a partition cannot answer a read shorter than k (its window may leave the slice)
+        lo = hi = 0xFFFFFFFFu;
+    } else {
+        search_read<QW, L>(a, P, m, lo, hi, steps, texts);
+    }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
     reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);

@@ -110,6 +110,7 @@ extern "C" sa_status sa_tree_create(const sa_index *idx, sa_tree **out) {
     if (!idx || !out) { sa_set_error("NULL argument"); return SA_EINVAL; }
     *out = nullptr;
     const uint64_t n = idx->n;
+    if (idx->nparts > 1) { sa_set_error("the tree needs a whole index, not a partition"); return SA_EINVAL; }
     if (n >= 0x7FFFFFFFull) { sa_set_error("the flattened tree needs n < 2^31 (leaf tag bit)"); return SA_ETOOLONG; }
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     // ---- LCP on the GPU ----

@@ -60,3 +60,47 @@ def combine(summaries: List[List[int]]) -> List[int]:
     if out[2] >= 1 << 63:
         out[2] -= 1 << 64
     return out
+
+
+def partitioned_match(idx, words, lens=None, fixed_len=None, out=None):
+    """match this rank's batch against a partitioned index (idx = this rank's part).
+
+    route (order by route key + rows in that order + per-destination offsets, sa_match_route) ->
+    all-to-all of the counts and of the rows -> match the received rows on this rank's slice ->
+    all-to-all of the intervals back -> sa_scatter_results into the batch's own order.  The
+    all-to-alls run over the default process group (NCCL on GPUs; gloo stages through host memory)."""
+    import paper_1303_3692_b200 as sa
+    Q, stride = words.shape
+    dev = words.device
+    order, ow, ol, offs = idx.route(words, lens, fixed_len=fixed_len)
+    offs = offs.cpu().tolist()
+    send = [offs[g + 1] - offs[g] for g in range(len(offs) - 1)]
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    if world != len(send):
+        raise ValueError(f"{len(send)} partitions but world size {world}")
+    host = world > 1 and dist.get_backend() != "nccl"
+    stage = (lambda t: t.cpu()) if host else (lambda t: t)
+    if world == 1:
+        recv, rows, rlens = send, ow, ol
+    else:
+        st = torch.tensor(send, dtype=torch.int64, device="cpu" if host else dev)
+        rt = torch.empty_like(st)
+        dist.all_to_all_single(rt, st)
+        recv = rt.cpu().tolist()
+        rows = torch.empty((sum(recv), stride), dtype=words.dtype, device="cpu" if host else dev)
+        dist.all_to_all_single(rows, stage(ow), output_split_sizes=recv, input_split_sizes=send)
+        rows = rows.to(dev)
+        rlens = None
+        if ol is not None:
+            rlens = torch.empty(sum(recv), dtype=ol.dtype, device="cpu" if host else dev)
+            dist.all_to_all_single(rlens, stage(ol), output_split_sizes=recv, input_split_sizes=send)
+            rlens = rlens.to(dev)
+    res = idx.match(rows, rlens, fixed_len=fixed_len) if rows.shape[0] else \
+        torch.empty((0, 2), dtype=torch.int32, device=dev)
+    if world == 1:
+        back = res
+    else:
+        back = torch.empty((Q, 2), dtype=torch.int32, device="cpu" if host else dev)
+        dist.all_to_all_single(back, stage(res), output_split_sizes=send, input_split_sizes=recv)
+        back = back.to(dev)
+    return sa.scatter_results(order, back, out=out)
