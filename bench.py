@@ -314,7 +314,6 @@ def main():
     streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(1 if chunks > 1 else 0)]
     bounds = [Q * c // chunks for c in range(chunks + 1)]
     ws_c = [ws] + [torch.empty_like(ws) for _ in range(1 if chunks > 1 else 0)]
-    ev_order = [torch.cuda.Event() for _ in range(chunks)]
 
     def step(i=None):
         # one pass of the hot path: [read ordering (a5)] -> bracket + joint lo/hi search + write (a6-a9)
