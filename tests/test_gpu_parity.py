@@ -180,6 +180,15 @@ def test_long_reads_generic_path():
         check_full(ref.tobytes(), words=words, lens=lens, layout=plain)
 
 
+@pytest.mark.parametrize("m_max", [160, 256])
+def test_reads_up_to_256_bases_in_registers(m_max):
+    # strides 5..8 words: the QW = 8 register path (two 256-bit row loads when aligned)
+    ref = synth.reference(synth.REF_REPEAT, 500_000, 31)
+    for layout in LAYOUTS:
+        words, lens = synth.reads(ref, 4000, 100, m_max, 0.1, 0.1, 32)
+        check_full(ref.tobytes(), words=words, lens=lens, layout=layout)
+
+
 def test_stats_iteration_bound():
     # SA_MATCH_STATS: steps per boundary search never exceed ceil(log2(n+2)); joint lo+hi <= 2x
     ref = synth.reference(synth.REF_REPEAT, 1_000_000, 41)
