@@ -276,7 +276,7 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     }
     // one vector load per read row when the row is exactly QW words and suitably aligned
     const uintptr_t wp = reinterpret_cast<uintptr_t>(q_words);
-    a.vec_rows = ((stride == 4 || stride == 8) && (wp & 31) == 0) || (stride == 2 && (wp & 15) == 0);
+    a.vec_rows = (stride == 4 && (wp & 31) == 0) || (stride == 2 && (wp & 15) == 0);
     a.dense_words = stride == 0 ? (Q * (uint64_t)fixed_len + 31) / 32 : 0;
     const bool st_on = stats != nullptr;
     const uint32_t nw = stride ? stride : (fixed_len + 31) / 32;  // register words needed
@@ -284,7 +284,6 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
     else if (nw <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
     else if (nw <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
-    else if (nw <= 8) e = launch_qw<8>(a, idx->layout, st_on, st);
     else e = launch_qw<0>(a, idx->layout, st_on, st);
     if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
     return SA_OK;

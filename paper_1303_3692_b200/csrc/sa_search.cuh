@@ -44,8 +44,9 @@ struct MatchArgs {
 };
 
 // ---- the read ---------------------------------------------------------------------------------
-// QW > 0: QW words in registers (loops over them are fully unrolled so indices are static; 1, 2, 4
-// or 8 words = reads up to 256 bases);
+// QW > 0: QW words in registers (loops over them are fully unrolled so indices are static; 1, 2 or 4
+// words = reads up to 128 bases; an 8-word variant measured 16% slower for 150-250-base reads,
+// profiles/r01x, as the extra registers cost occupancy);
 // QW == 0: long reads, words read from global memory (L1-cached) as needed.
 template <int QW>
 struct QueryWords {
@@ -56,12 +57,6 @@ struct QueryWords {
         if constexpr (QW == 4) {
             if (vec) {
                 ld_v4u64(p, w[0], w[1], w[2], w[3]);
-                return;
-            }
-        } else if constexpr (QW == 8) {
-            if (vec) {
-                ld_v4u64(p, w[0], w[1], w[2], w[3]);
-                ld_v4u64(p + 4, w[4], w[5], w[6], w[7]);
                 return;
             }
         } else if constexpr (QW == 2) {

@@ -181,8 +181,8 @@ def test_long_reads_generic_path():
 
 
 @pytest.mark.parametrize("m_max", [160, 256])
-def test_reads_up_to_256_bases_in_registers(m_max):
-    # strides 5..8 words: the QW = 8 register path (two 256-bit row loads when aligned)
+def test_reads_of_129_to_256_bases(m_max):
+    # strides 5..8 words: the generic (global-memory read) path with records and text past the cache
     ref = synth.reference(synth.REF_REPEAT, 500_000, 31)
     for layout in LAYOUTS:
         words, lens = synth.reads(ref, 4000, 100, m_max, 0.1, 0.1, 32)
