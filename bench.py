@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--layout", default="rec32", choices=["rec16", "rec32", "plain"],
                     help="SA layout: 16-byte records caching 48 bases (default), 32-byte records caching 112 "
                          "bases, or a plain uint32 SA")
+    ap.add_argument("--subtables", action="store_true",
+                    help="second-level (k+4)-base tables for k-mer buckets of > 32 suffixes (SA_INDEX_SUBTABLE)")
     ap.add_argument("--build", default="doubling", choices=["doubling", "dc3"],
                     help="suffix-array construction (untimed): prefix doubling or the paper's DC3")
     ap.add_argument("--no-order", action="store_true", help="skip the read-ordering step (a5)")
@@ -276,7 +278,8 @@ def main():
     log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
     t0 = time.time()
     part = (rank, world, 12) if args.partition else None
-    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build, part=part)
+    idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build, part=part,
+                   subtables=args.subtables)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     log(f"index built in {build_s:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")

@@ -83,6 +83,10 @@ typedef struct {
  * Sec. III; on the GPU: radix-sorted sample triples, recursion on the reduced string, merge-path
  * merge) instead of the default prefix doubling.  Same SA (it is unique); a different build cost. */
 #define SA_INDEX_BUILD_DC3 4u
+/* sa_index_opts.flags: k-mer buckets holding more than 32 suffixes (repeats) get a second-level
+ * bracket table over the next 4 bases (257 SA ranks each, found through a hash of the k-mer), so
+ * reads of >= k+4 bases in such a bucket start from a bracket ~256x smaller. */
+#define SA_INDEX_SUBTABLE 8u
 
 /* sa_match_batch flags. */
 #define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace:

@@ -29,6 +29,8 @@ static void free_index(sa_index *idx) {
     cudaFree(idx->sa);
     cudaFree(idx->rec);
     cudaFree(idx->table);
+    cudaFree(idx->big_hash);
+    cudaFree(idx->big_sub);
     for (int b = 0; b < 2; ++b) {
         cudaFree(idx->pipe_words[b]);
         cudaFree(idx->pipe_lens[b]);
@@ -52,7 +54,7 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     }
     sa_index_opts o{-1, 0, 0, 0};
     if (opts) o = *opts;
-    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32 | SA_INDEX_BUILD_DC3)) != 0 ||
+    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32 | SA_INDEX_BUILD_DC3 | SA_INDEX_SUBTABLE)) != 0 ||
         (o.flags & (SA_INDEX_PLAIN | SA_INDEX_REC32)) == (SA_INDEX_PLAIN | SA_INDEX_REC32) || o.reserved != 0) {
         sa_set_error("unknown opts.flags bits / reserved must be 0");
         return SA_EINVAL;
@@ -78,6 +80,7 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     idx->n = n;
     idx->layout = (o.flags & SA_INDEX_PLAIN) ? 0 : (o.flags & SA_INDEX_REC32) ? 2 : 1;
     idx->build_dc3 = (o.flags & SA_INDEX_BUILD_DC3) != 0;
+    idx->subtables = (o.flags & SA_INDEX_SUBTABLE) != 0;
     uint32_t k = o.kmer_k;
     if (k == 0) {  // auto: floor(log4 n) + 1 (mean bracket < 1 suffix), at most 16 (a 16 GiB table)
         k = 1;

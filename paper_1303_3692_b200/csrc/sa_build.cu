@@ -14,6 +14,7 @@
 // so s + h <= n and rank[] needs only one extra slot.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <cstring>
 #include <vector>
@@ -143,6 +144,45 @@ __global__ void k_table(const uint64_t *__restrict__ text, uint64_t n, const uin
         const int64_t lo = (r == 0) ? 0 : kmer_e(text, n, sa, r - 1, k) + 1;
         const int64_t hi = (r == n) ? K : kmer_e(text, n, sa, r, k);
         for (int64_t x = lo; x <= hi; ++x) T[x] = (uint32_t)r;
+    }
+}
+
+// ---- second-level tables for large buckets (SA_INDEX_SUBTABLE) ------------------------------------
+// A bucket x with more than kBigBucket suffixes gets T2_x[y] = #{i : trunc_{k+4}(S_i) < x.y} for the
+// 256 extensions y of x by 4 bases (+1 entry): the k+4 bracket table restricted to that bucket.
+struct IsBigBucket {
+    const uint32_t *T;
+    __host__ __device__ int64_t operator()(uint32_t x) const { return T[(uint64_t)x + 1] - T[x] > kBigBucket ? 1 : 0; }
+};
+
+__device__ __forceinline__ uint64_t big_hash(uint32_t x, uint32_t bits) {
+    return (uint64_t)((x * 0x9E3779B1u) >> (32 - bits));
+}
+
+__global__ void k_big_hash_insert(const uint32_t *__restrict__ big, uint64_t cnt, uint32_t bits, uint2 *__restrict__ H) {
+    GRID_STRIDE(id, cnt) {
+        const uint32_t x = big[id];
+        const uint64_t mask = (1ull << bits) - 1;
+        for (uint64_t h = big_hash(x, bits);; h = (h + 1) & mask) {
+            const unsigned prev = atomicCAS(&H[h].x, 0xFFFFFFFFu, x);
+            if (prev == 0xFFFFFFFFu) { H[h].y = (uint32_t)id; break; }
+        }
+    }
+}
+
+// one block per big bucket: T2[y] = r for e(r-1) < x.y <= e(r), r over the bucket's ranks
+__global__ void k_big_subtables(const uint64_t *__restrict__ text, uint64_t n, const uint32_t *__restrict__ sa,
+                                unsigned k, const uint32_t *__restrict__ T, const uint32_t *__restrict__ big,
+                                uint32_t *__restrict__ sub) {
+    const uint32_t x = big[blockIdx.x];
+    uint32_t *T2 = sub + (uint64_t)blockIdx.x * 257;
+    const uint64_t r0 = T[x], r1 = T[(uint64_t)x + 1];
+    const int64_t base = (int64_t)x << 8;
+    for (uint64_t r = r0 + threadIdx.x; r <= r1; r += blockDim.x) {
+        const int64_t lo = (r == r0) ? 0 : kmer_e(text, n, sa, r - 1, k + 4) - base + 1;
+        const int64_t hi = (r == r1) ? 256 : kmer_e(text, n, sa, r, k + 4) - base;
+        const int64_t a = lo < 0 ? 0 : lo, b = hi > 256 ? 256 : hi;
+        for (int64_t y = a; y <= b; ++y) T2[y] = (uint32_t)r;
     }
 }
 
@@ -377,6 +417,55 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
     SA_CUDA_TRY(cudaMalloc(&idx->table, (K + 1) * sizeof(uint32_t)));
     k_table<<<grid_for(n + 1), kThreads, 0, st>>>(idx->text, n, idx->sa, idx->k, idx->table);
     SA_CUDA_TRY(cudaGetLastError());
+    // ---- 3b. second-level tables for the large buckets (SA_INDEX_SUBTABLE) ----
+    if (idx->subtables && idx->k + 4 <= 32) {
+        // count, then select, the large buckets (chunks of 2^30 k-mers)
+        thrust::counting_iterator<uint32_t> xs(0);
+        const uint64_t CH = 1ull << 30;
+        DevBuf<int64_t> cnt;
+        SA_TRY(cnt.alloc(1, st, "big bucket count"));
+        thrust::transform_iterator<IsBigBucket, thrust::counting_iterator<uint32_t>, int64_t> flag(xs, IsBigBucket{idx->table});
+        int64_t total = 0;
+        for (uint64_t x0 = 0; x0 < K; x0 += CH) {
+            const uint64_t len = (K - x0 < CH) ? K - x0 : CH;
+            SA_TRY(cub_call([&](void *tmp, size_t &bytes) {
+                return cub::DeviceReduce::Sum(tmp, bytes, flag + x0, cnt.p, (int64_t)len, st);
+            }, st, "big bucket count"));
+            int64_t c = 0;
+            SA_CUDA_TRY(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            total += c;
+        }
+        if (total > 0 && total < (1ll << 26)) {
+            DevBuf<uint32_t> big;
+            SA_TRY(big.alloc((uint64_t)total, st, "big buckets"));
+            int64_t off = 0;
+            for (uint64_t x0 = 0; x0 < K; x0 += CH) {
+                const uint64_t len = (K - x0 < CH) ? K - x0 : CH;
+                SA_TRY(cub_call([&](void *tmp, size_t &bytes) {
+                    return cub::DeviceSelect::If(tmp, bytes, xs + x0, big.p + off, cnt.p, (int64_t)len,
+                                                 IsBigBucket{idx->table}, st);
+                }, st, "big bucket select"));
+                int64_t c = 0;
+                SA_CUDA_TRY(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+                SA_CUDA_TRY(cudaStreamSynchronize(st));
+                off += c;
+            }
+            uint32_t bits = 1;
+            while ((1ull << bits) < 2ull * (uint64_t)total) ++bits;
+            SA_CUDA_TRY(cudaMalloc(&idx->big_sub, (uint64_t)total * 257 * sizeof(uint32_t)));
+            SA_CUDA_TRY(cudaMalloc(&idx->big_hash, (1ull << bits) * sizeof(uint2)));
+            SA_CUDA_TRY(cudaMemsetAsync(idx->big_hash, 0xFF, (1ull << bits) * sizeof(uint2), st));
+            k_big_hash_insert<<<grid_for((uint64_t)total), kThreads, 0, st>>>(big.p, (uint64_t)total, bits, idx->big_hash);
+            SA_CUDA_TRY(cudaGetLastError());
+            k_big_subtables<<<(unsigned)total, 128, 0, st>>>(idx->text, n, idx->sa, idx->k, idx->table, big.p,
+                                                            idx->big_sub);
+            SA_CUDA_TRY(cudaGetLastError());
+            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            idx->big_count = (uint64_t)total;
+            idx->big_bits = bits;
+        }
+    }
     // ---- 4. SA records (default layout) ----
     uint64_t sa_bytes = n * sizeof(uint32_t);
     if (idx->layout != 0) {
@@ -393,7 +482,8 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
         sa_bytes = n * per * sizeof(uint4);
     }
     SA_CUDA_TRY(cudaStreamSynchronize(st));
-    idx->device_bytes = idx->n_words * 8 + sa_bytes + (K + 1) * 4;
+    idx->device_bytes = idx->n_words * 8 + sa_bytes + (K + 1) * 4 + idx->big_count * 257 * 4 +
+                        (idx->big_count ? (1ull << idx->big_bits) * 8 : 0);
     // hand the build's transient memory back to the driver
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);

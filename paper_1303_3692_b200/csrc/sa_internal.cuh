@@ -71,6 +71,7 @@ struct DevBuf {
 
 // ---------------------------------------------------------------------------------------------
 // the index (immutable after create)
+constexpr uint32_t kBigBucket = 32;  // SA_INDEX_SUBTABLE threshold (suffixes per k-mer bucket)
 constexpr uint64_t kGuardWords = 6;  // zero words past the text: windows up to base n + 159 are readable
 
 // SA values of the layout: base pointer + stride in uint32 units
@@ -91,6 +92,12 @@ struct sa_index {
     uint64_t device_bytes = 0;
     uint32_t build_rounds = 0;   // prefix-doubling rounds after the initial sort
     bool build_dc3 = false;      // SA_INDEX_BUILD_DC3: the SA by DC3 instead of prefix doubling
+    // SA_INDEX_SUBTABLE: buckets of more than kBigBucket suffixes get a (k+4)-base sub-table
+    bool subtables = false;
+    uint64_t big_count = 0;      // large buckets
+    uint32_t big_bits = 0;       // log2 of the hash table size
+    uint2 *big_hash = nullptr;   // dev: open addressing {bucket x, sub-table id}, empty = {~0, ~0}
+    uint32_t *big_sub = nullptr; // dev: big_count x 257 global SA ranks
     // partitioned index (sa_index_create_part): this index holds SA ranks [rank_base, rank_end) and
     // table entries [x_base, x_end] only, i.e. the reads whose first route_bases bases lie in
     // [part_keys[part], part_keys[part+1])
@@ -138,6 +145,11 @@ __device__ __forceinline__ uint64_t ld_u64(const uint64_t *p) {
 __device__ __forceinline__ uint4 ld_v4u32(const void *p) {
     uint4 v;
     asm(SA_LD_OP ".v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_v2u32(const void *p) {
+    uint2 v;
+    asm(SA_LD_OP ".v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
 __device__ __forceinline__ void ld_v2u64(const void *p, uint64_t &a, uint64_t &b) {

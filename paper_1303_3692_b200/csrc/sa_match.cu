@@ -266,6 +266,9 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.stats = stats;
     a.order = order;
     a.min_len = 0;
+    a.big_hash = idx->big_hash;
+    a.big_sub = idx->big_sub;
+    a.big_bits = idx->big_bits;
     if (idx->nparts > 1) {
         // a partition holds table entries [x_base, x_end] and SA ranks [rank_base, rank_end): address them
         // with their global indices through shifted base pointers (only in-slice indices are dereferenced)

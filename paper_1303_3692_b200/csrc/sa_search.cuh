@@ -41,6 +41,9 @@ struct MatchArgs {
     uint64_t dense_words;               // stride == 0: dense layout, words = one 2-bit stream of this many words
     bool rows_ordered;                  // SA_MATCH_ROWS_ORDERED: row t is read order[t]
     uint32_t min_len;                   // partitioned index: reads shorter than k get (~0, ~0)
+    const uint2 *__restrict__ big_hash; // SA_INDEX_SUBTABLE: {bucket, sub-table id}, empty = {~0, ~0}
+    const uint32_t *__restrict__ big_sub;
+    uint32_t big_bits;
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -324,6 +327,22 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
     const uint64_t x = P.first() >> (64 - 2 * k);
     uint32_t Lp1, R;
     table_pair(a.table, x, Lp1, R);
+    if (a.big_sub && R - Lp1 > kBigBucket && m >= k + 4) {
+        // a large bucket (repeats): its (k+4)-base sub-table narrows the bracket by the next 4 bases
+        const uint64_t mask = (1ull << a.big_bits) - 1;
+        uint64_t h = (uint64_t)(((uint32_t)x * 0x9E3779B1u) >> (32 - a.big_bits));
+        for (uint64_t tries = 0; tries <= mask; ++tries, h = (h + 1) & mask) {
+            const uint2 e = ld_v2u32(a.big_hash + h);
+            if (e.x == (uint32_t)x) {
+                const uint32_t *T2 = a.big_sub + (uint64_t)e.y * 257;
+                const uint32_t y = (uint32_t)(read_after_k<QW>(P, k, 0) >> 56);  // bases k .. k+3
+                Lp1 = ld_u32(T2 + y);
+                R = ld_u32(T2 + y + 1);
+                break;
+            }
+            if (e.x == 0xFFFFFFFFu) break;
+        }
+    }
     uint32_t lcpL = 0, lcpR = 0;
     uint32_t hLp1 = 0, hR = 0, hlcpL = 0, hlcpR = 0;
     bool split = false;

@@ -38,10 +38,10 @@ def gpu_match(idx, words, lens=None, fixed_len=None, presort=False, want_stats=F
 LAYOUTS = ["rec16", "rec32", "plain"]
 
 
-def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, layout="rec16"):
+def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, layout="rec16", subtables=False):
     """Build on the GPU; compare SA, table and every interval with the oracle."""
     S = oracle.encode(text_ascii)
-    idx = sa.Index(text_ascii, k=k, layout=layout)
+    idx = sa.Index(text_ascii, k=k, layout=layout, subtables=subtables)
     sa_ref = oracle.sa_naive(S)
     if check_sa:
         assert np.array_equal(idx.export_sa(), sa_ref)
@@ -121,6 +121,22 @@ def test_random_texts_all_k(n, k, plain):
 def test_periodic_and_homopolymer_texts(text, plain):
     rng = random.Random(len(text))
     check_full(text, hazard_queries(text, 8, rng), k=8, layout=plain)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_subtables_for_large_buckets(k, layout):
+    # small k on a few-kbp text: most buckets exceed 32 suffixes, so the (k+4)-base sub-tables are used
+    rng = random.Random(k)
+    for n in [3000, 20000]:
+        text = "".join(rng.choice("ACGT") for _ in range(n)) + "A" * 300 + "AC" * 200
+        check_full(text, hazard_queries(text, k, rng, extra=400), k=k, layout=layout, subtables=True)
+
+
+def test_subtables_repeat_rich():
+    ref = synth.reference(synth.REF_REPEAT, 3_000_000, 35)
+    words, lens = synth.reads(ref, 200_000, 16, 160, 0.1, 0.01, 36)
+    check_full(ref.tobytes(), words=words, lens=lens, layout="rec32", subtables=True)
 
 
 def test_homopolymer_closed_form():
