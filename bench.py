@@ -467,8 +467,7 @@ def main():
         torch.cuda.synchronize()
         l1b = torch.cuda.Event(enable_timing=True)
         l1b.record(stream)
-        sa._check(sa.lib().sa_locate(idx._h, out.data_ptr(), offs.data_ptr(), n_loc, pos.data_ptr() or None,
-                                     stream.cuda_stream or None), "sa_locate")
+        idx.locate_positions(out, offs, n_reads=n_loc, stream=stream, out=pos)
         l2.record(stream)
         torch.cuda.synchronize()
         npos = int(pos.numel())

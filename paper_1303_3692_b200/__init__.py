@@ -306,12 +306,14 @@ class Index:
                                        _stream_ptr(stream)), "sa_locate_offsets")
         return offsets
 
-    def locate_positions(self, lohi, offsets, n_reads: Optional[int] = None, stream=None):
-        """sa_locate over the first n_reads reads (default all): positions SA[lo..hi) in SA order, int32 [total]."""
+    def locate_positions(self, lohi, offsets, n_reads: Optional[int] = None, stream=None, out=None):
+        """sa_locate over the first n_reads reads (default all): positions SA[lo..hi) in SA order, int32 [total].
+        out: optional preallocated int32 tensor of >= offsets[n_reads] entries."""
         import torch
         Q = lohi.shape[0] if n_reads is None else int(n_reads)
-        total = int(offsets[Q].item())
-        positions = torch.empty(total, dtype=torch.int32, device=lohi.device)
+        if out is None:
+            out = torch.empty(int(offsets[Q].item()), dtype=torch.int32, device=lohi.device)
+        positions = out
         _check(lib().sa_locate(self._h, _dptr(lohi), _dptr(offsets), Q, _dptr(positions), _stream_ptr(stream)),
                "sa_locate")
         return positions
