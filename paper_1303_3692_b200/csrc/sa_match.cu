@@ -155,8 +155,12 @@ struct CountOp {
     }
 };
 
-// One warp per query: lanes copy SA[lo .. hi) to positions[off ..] (contiguous, coalesced).
-// SA values are read through the layout's view (stride 1 = plain SA, 4 = 16-byte records).
+// Locate, load-balanced in two parts.  Reads with at most kHeavy occurrences: one warp per read, lanes
+// copy SA[lo .. hi) to positions[off ..] (contiguous, coalesced).  Heavier reads (repeats: up to 10^6
+// occurrences) are cut into chunks of kHeavy positions and every chunk is copied by a whole block.
+// SA values are read through the layout's view (stride 1 = plain SA, 4 / 8 = 16- / 32-byte records).
+constexpr uint32_t kHeavy = 4096;
+
 __global__ void k_locate(const uint32_t *__restrict__ sa, uint32_t sa_stride, const uint32_t *__restrict__ lohi,
                          const uint64_t *__restrict__ offsets, uint64_t Q, uint32_t *__restrict__ pos) {
     const unsigned lane = threadIdx.x & 31;
@@ -164,8 +168,49 @@ __global__ void k_locate(const uint32_t *__restrict__ sa, uint32_t sa_stride, co
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t q = warp; q < Q; q += nwarps) {
         const uint32_t lo = lohi[2 * q], hi = lohi[2 * q + 1];
+        if (hi - lo > kHeavy) continue;  // the chunked kernel copies it
         const uint64_t off = offsets[q];
         for (uint64_t j = lane; j < (uint64_t)(hi - lo); j += 32) pos[off + j] = __ldg(sa + (lo + j) * sa_stride);
+    }
+}
+
+struct ChunksOfRead {  // chunks of kHeavy positions of a heavy read (0 for the others)
+    const uint32_t *lohi;
+    __host__ __device__ uint64_t operator()(uint64_t q) const {
+        const uint32_t c = lohi[2 * q + 1] - lohi[2 * q];
+        return c > kHeavy ? (c + kHeavy - 1) / kHeavy : 0;
+    }
+};
+
+// chunk_off[Q] = chunk_off[Q-1] + chunks of read Q-1 (the total)
+__global__ void k_chunk_total(const uint32_t *__restrict__ lohi, uint64_t Q, uint64_t *__restrict__ chunk_off) {
+    const uint32_t c = lohi[2 * (Q - 1) + 1] - lohi[2 * (Q - 1)];
+    chunk_off[Q] = chunk_off[Q - 1] + (c > kHeavy ? (c + kHeavy - 1) / kHeavy : 0);
+}
+
+// block b copies chunk b (grid-stride): find its read by binary search over the chunk offsets
+__global__ void k_locate_heavy(const uint32_t *__restrict__ sa, uint32_t sa_stride, const uint32_t *__restrict__ lohi,
+                               const uint64_t *__restrict__ offsets, uint64_t Q, const uint64_t *__restrict__ chunk_off,
+                               uint32_t *__restrict__ pos) {
+    const uint64_t nchunks = chunk_off[Q];
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        __shared__ uint64_t s_q;
+        if (threadIdx.x == 0) {
+            uint64_t a = 0, b = Q;  // last q with chunk_off[q] <= c
+            while (b - a > 1) {
+                const uint64_t mid = (a + b) >> 1;
+                if (chunk_off[mid] <= c) a = mid; else b = mid;
+            }
+            s_q = a;
+        }
+        __syncthreads();
+        const uint64_t q = s_q;
+        __syncthreads();
+        const uint32_t lo = lohi[2 * q], hi = lohi[2 * q + 1];
+        const uint64_t j0 = (c - chunk_off[q]) * kHeavy;
+        const uint64_t j1 = j0 + kHeavy < (uint64_t)(hi - lo) ? j0 + kHeavy : (uint64_t)(hi - lo);
+        const uint64_t off = offsets[q];
+        for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) pos[off + j] = __ldg(sa + (lo + j) * sa_stride);
     }
 }
 
@@ -480,10 +525,27 @@ extern "C" sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, co
     // positions may be NULL only when offsets[Q] == 0 (nothing is written then)
     if (!out_lohi || !offsets) { sa_set_error("NULL argument"); return SA_EINVAL; }
     SA_CUDA_TRY(cudaSetDevice(idx->device));
+    cudaStream_t st = (cudaStream_t)stream;
     uint64_t blocks = (Q * 32 + 255) / 256;
     if (blocks > 148ull * 32) blocks = 148ull * 32;
     const SaView v = sa_view(idx);
-    k_locate<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(v.base, v.stride, out_lohi, offsets, Q, positions);
+    k_locate<<<(unsigned)blocks, 256, 0, st>>>(v.base, v.stride, out_lohi, offsets, Q, positions);
+    SA_CUDA_TRY(cudaGetLastError());
+    // heavy reads: exclusive scan of their chunk counts, then one block per chunk
+    DevBuf<uint64_t> chunk_off;
+    SA_TRY(chunk_off.alloc(Q + 1, st, "locate chunk offsets"));
+    ChunksOfRead op{out_lohi};
+    thrust::transform_iterator<ChunksOfRead, thrust::counting_iterator<uint64_t>, uint64_t> it(
+        thrust::counting_iterator<uint64_t>(0), op);
+    size_t bytes = 0;
+    SA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, chunk_off.p, (int64_t)(Q + 1), st));
+    DevBuf<uint8_t> tmp;
+    SA_TRY(tmp.alloc(bytes, st, "locate scan"));
+    // (entry Q of the transform reads lohi[2Q]: the scan input must stop at Q, so scan Q items and fix up)
+    SA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, it, chunk_off.p, (int64_t)Q, st));
+    k_chunk_total<<<1, 1, 0, st>>>(out_lohi, Q, chunk_off.p);
+    SA_CUDA_TRY(cudaGetLastError());
+    k_locate_heavy<<<148 * 16, 256, 0, st>>>(v.base, v.stride, out_lohi, offsets, Q, chunk_off.p, positions);
     SA_CUDA_TRY(cudaGetLastError());
     return SA_OK;
 }

@@ -325,6 +325,20 @@ def test_locate_parity(plain):
         assert np.array_equal(pos[offs[q]:offs[q + 1]], oracle.locate(sa_ref, int(got[q, 0]), int(got[q, 1])))
 
 
+@pytest.mark.parametrize("plain", LAYOUTS)
+def test_locate_heavy_reads(plain):
+    # reads with > 4096 occurrences take the chunked (block per 4096 positions) path
+    text = "A" * 30000 + "ACGT" * 3000 + "".join(random.Random(3).choice("ACGT") for _ in range(5000))
+    qs = ["A" * m for m in (1, 3, 7, 100, 5000)] + ["ACGT", "AC", "GTA", "T", "CCCC"]
+    idx, S, sa_ref, got = check_full(text, qs, layout=plain, k=6)
+    offs, pos = idx.locate(torch.from_numpy(got.view(np.int32)).cuda())
+    offs = offs.cpu().numpy()
+    pos = pos.cpu().numpy().view(np.uint32)
+    assert (got[:, 1].astype(np.int64) - got[:, 0]).max() > 4096
+    for q in range(len(qs)):
+        assert np.array_equal(pos[offs[q]:offs[q + 1]], oracle.locate(sa_ref, int(got[q, 0]), int(got[q, 1])))
+
+
 def _full_size_check(cfg, sample=2000, q_count=None, layout="rec32"):
     """The bench configuration (bench.py defaults: rec32 records, auto k, reads ordered by 12 bases)."""
     ref = cfg.reference()
