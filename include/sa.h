@@ -180,7 +180,8 @@ sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_
  * device's memory.  Allocates buffer_bytes, then every thread issues `loads`
  * independent (dependent=0) or pointer-chased (dependent=1) loads -- or, with dependent=2,
  * independent stores; 10..13: independent loads with the PTX cache operator .nc / .cg / .cv /
- * .nc.L1::no_allocate (access_bytes 8 or 32) -- of
+ * .nc.L1::no_allocate (access_bytes 8 or 32); 20..22 (access_bytes 32): TMA bulk copies into
+ * shared memory, cp.async.cg (LDGSTS), ld.global.nc.L2::64B -- of
  * access_bytes (4, 8, 16 or 32) at hashed, access_bytes-aligned offsets.
  * *ms = device time of one launch of n_threads threads (CUDA events). */
 sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,

@@ -383,7 +383,8 @@ def dc3_trace(ref):
 
 def random_gather(device: int = 0, buffer_bytes: int = 16 << 30, access_bytes: int = 32, n_threads: int = 148 * 2048 * 4,
                   loads: int = 64, dependent: int = 0) -> dict:
-    """Random-access microbenchmark: dependent=0 independent loads, 1 pointer-chased loads, 2 stores."""
+    """Random-access microbenchmark: dependent=0 independent loads, 1 pointer-chased loads, 2 stores,
+    10-13 PTX cache operators, 20 TMA bulk copies, 21 cp.async (LDGSTS), 22 the L2::64B hint (32-B accesses)."""
     ms = ctypes.c_float()
     _check(lib().sa_tool_random_gather(device, buffer_bytes, access_bytes, n_threads, loads, int(dependent),
                                        ctypes.byref(ms)), "sa_tool_random_gather")

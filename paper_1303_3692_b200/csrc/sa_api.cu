@@ -348,6 +348,74 @@ __global__ void k_gather_op(const uint8_t *__restrict__ buf, uint64_t slot_mask,
     if (acc == 0x5eed) sink[0] = acc;
 }
 
+// modes 20..22: the same 32-byte random loads through the asynchronous copy paths, to see whether a
+// path that is not an LSU load moves fewer than the 4 DRAM sectors an LSU load costs:
+// 20 cp.async.bulk (TMA bulk copy, 32 B into shared memory, mbarrier completion), 21 cp.async.cg
+// (LDGSTS, two 16-byte copies), 22 ld.global.nc.L2::64B (prefetch-size hint).
+template <int OP>
+__global__ void __launch_bounds__(128) k_gather_async(const uint8_t *__restrict__ buf, uint64_t slot_mask,
+                                                      uint32_t loads, uint64_t *__restrict__ sink) {
+    __shared__ __align__(128) ulonglong4 stage[128 * 8];
+    __shared__ __align__(8) uint64_t bar[4];
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[warp]);
+    if constexpr (OP == 20) {
+        if (lane == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+    }
+    ulonglong4 *mine = stage + threadIdx.x * 8;
+    uint64_t acc = 0;
+    uint32_t phase = 0;
+    const uint64_t h = hash64(tid * 0x9E3779B97F4A7C15ull + 0x1234567ull);
+    for (uint32_t i = 0; i < loads; i += 8) {
+        if constexpr (OP == 22) {
+            uint64_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint8_t *p = buf + (hash64(h + i + u) & slot_mask) * 32;
+                uint64_t a, c, d, e;
+                asm volatile("ld.global.nc.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                             : "=l"(a), "=l"(c), "=l"(d), "=l"(e) : "l"(p));
+                v[u] = a ^ c ^ d ^ e;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
+            continue;
+        }
+        if constexpr (OP == 20) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(8 * 32) : "memory");
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint8_t *p = buf + (hash64(h + i + u) & slot_mask) * 32;
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(mine + u);
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32, [%2];"
+                             ::"r"(dst), "l"(p), "r"(b) : "memory");
+            }
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile("{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2; selp.u32 %0, 1, 0, P; }"
+                             : "=r"(done) : "r"(b), "r"(phase) : "memory");
+            }
+            phase ^= 1;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint8_t *p = buf + (hash64(h + i + u) & slot_mask) * 32;
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(mine + u);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(p) : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16), "l"(p + 16) : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += mine[u].x ^ mine[u].w;
+        __syncwarp();
+    }
+    if (acc == 0x5eed) sink[0] = acc + lane;
+}
+
 // mode 2: random stores of BYTES (partial-sector stores below 32 B exercise the L2 / ECC
 // read-modify-write path of a scattered result write)
 template <int BYTES>
@@ -406,6 +474,13 @@ extern "C" sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes
                 if (op == 0) SA_GOP(8, 0); else if (op == 1) SA_GOP(8, 1); else if (op == 2) SA_GOP(8, 2); else SA_GOP(8, 3);
             }
 #undef SA_GOP
+            return;
+        }
+        if (dependent >= 20 && dependent <= 22 && access_bytes == 32) {
+            const unsigned b2 = blocks * 2;  // 128-thread blocks (64 KB of staging would not fit otherwise)
+            if (dependent == 20) k_gather_async<20><<<b2, 128>>>(buf, slots - 1, loads, sink);
+            else if (dependent == 21) k_gather_async<21><<<b2, 128>>>(buf, slots - 1, loads, sink);
+            else k_gather_async<22><<<b2, 128>>>(buf, slots - 1, loads, sink);
             return;
         }
         if (dependent == 2) {

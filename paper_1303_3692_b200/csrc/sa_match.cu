@@ -23,6 +23,26 @@ cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// long reads: G lanes per read (sa_search::k_match_group)
+template <int G, int WPL, int L, bool STATS>
+cudaError_t launch_g(const MatchArgs &a, cudaStream_t st) {
+    const int threads = 256;
+    const uint64_t blocks = (a.Q * G + threads - 1) / threads;
+    if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
+    sa_search::k_match_group<G, WPL, L, STATS><<<(unsigned)blocks, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int G, int WPL>
+cudaError_t launch_group(const MatchArgs &a, int layout, bool stats, cudaStream_t st) {
+    using namespace sa_search;
+    switch (layout) {
+    case L_PLAIN: return stats ? launch_g<G, WPL, L_PLAIN, true>(a, st) : launch_g<G, WPL, L_PLAIN, false>(a, st);
+    case L_REC32: return stats ? launch_g<G, WPL, L_REC32, true>(a, st) : launch_g<G, WPL, L_REC32, false>(a, st);
+    default: return stats ? launch_g<G, WPL, L_REC16, true>(a, st) : launch_g<G, WPL, L_REC16, false>(a, st);
+    }
+}
+
 template <int QW>
 cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t st) {
     using namespace sa_search;
@@ -329,10 +349,18 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     const bool st_on = stats != nullptr;
     const uint32_t nw = stride ? stride : (fixed_len + 31) / 32;  // register words needed
     cudaError_t e;
+    // reads of more than 4 words: G = 8 / 16 / 32 lanes per read (SA_MATCH_NO_GROUP=1: one thread per
+    // read, words from global memory -- the A/B baseline of DESIGN.md §7)
+    static const bool no_group = getenv("SA_MATCH_NO_GROUP") && atoi(getenv("SA_MATCH_NO_GROUP")) != 0;
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
     else if (nw <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
     else if (nw <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
-    else e = launch_qw<0>(a, idx->layout, st_on, st);
+    else if (no_group) e = launch_qw<0>(a, idx->layout, st_on, st);
+    else if (nw <= 8) e = launch_group<8, 1>(a, idx->layout, st_on, st);
+    else if (nw <= 16) e = launch_group<16, 1>(a, idx->layout, st_on, st);
+    else if (nw <= 32) e = launch_group<32, 1>(a, idx->layout, st_on, st);
+    else if (nw <= 64) e = launch_group<32, 2>(a, idx->layout, st_on, st);
+    else e = launch_group<32, 0>(a, idx->layout, st_on, st);
     if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
     return SA_OK;
 }

@@ -207,6 +207,9 @@ __device__ __forceinline__ uint64_t read_after_k(const QueryWords<QW> &P, uint32
     return (P.word(j) << (2 * k)) | (P.word(j + 1) >> (64 - 2 * k));
 }
 
+template <int QW>
+__device__ __forceinline__ uint64_t after_k0(const QueryWords<QW> &P, uint32_t k) { return read_after_k<QW>(P, k, 0); }
+
 // Compare P (m >= k, inside its k-mer bracket) with the suffix of a record.  Every suffix with >= k
 // bases in the bracket starts with P's k-mer, so the compare starts at base k on the cached bases;
 // the text is read only when all cached bases are equal and more remain, or for the < k suffixes
@@ -279,24 +282,186 @@ __device__ __forceinline__ void compare_probe(const MatchArgs &a, const Probe<L>
     }
 }
 
-template <int QW, int L>
-__device__ __forceinline__ void probe(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint64_t p,
+// ---- group-cooperative reads (long reads, m > 128) ---------------------------------------------
+// G lanes (8, 16 or 32) hold one read: word j of P sits in lane j % G (WPL words per lane in
+// registers; WPL == 0: read from global memory when needed).  One compare step covers G words (32·G
+// bases): every lane compares its own word with the text (adjacent lanes, adjacent text words: one
+// coalesced request), __ballot_sync over the group finds the first differing word and __shfl_sync
+// broadcasts its lcp and sign (north_star's warp-cooperative compare).  A 1000-base compare is one
+// round trip instead of ~30 dependent ones; the search's control state stays uniform in the group.
+template <int G, int WPL>
+struct GroupRead {
+    static constexpr int kRegs = WPL > 0 ? WPL : 1;
+    uint64_t w[kRegs];       // w[i] = word lane + G*i of P (0 past the read)
+    uint64_t w0, w1;         // words 0 and 1, in every lane
+    const uint64_t *p;       // the row
+    unsigned sh;             // dense layout: bit shift of the read inside its first word
+    uint64_t left;           // dense layout: words readable from p
+    uint32_t nw;             // words of the read
+    unsigned lane, base, mask;  // lane in the group, the group's first lane in the warp, its lane mask
+
+    __device__ __forceinline__ uint64_t raw(uint64_t j) const { return j < left ? ld_u64(p + j) : 0ull; }
+    __device__ __forceinline__ uint64_t gword(uint32_t j) const {
+        if (j >= nw) return 0ull;
+        return sh ? (raw(j) << sh) | (raw(j + 1) >> (64 - sh)) : raw(j);
+    }
+    __device__ __forceinline__ uint64_t own(int i) const {  // word lane + G*i
+        if constexpr (WPL > 0) return w[i];
+        else return gword(lane + G * (uint32_t)i);
+    }
+    __device__ __forceinline__ void init(const uint64_t *row, unsigned shift, uint64_t readable, uint32_t n) {
+        p = row;
+        sh = shift;
+        left = readable;
+        nw = n;
+        lane = threadIdx.x & (G - 1);
+        base = (threadIdx.x & 31) & ~(G - 1);
+        mask = G == 32 ? 0xFFFFFFFFu : (((1u << (G & 31)) - 1) << base);
+#pragma unroll
+        for (int i = 0; i < kRegs; ++i) w[i] = gword(lane + G * i);
+        w0 = __shfl_sync(mask, w[0], 0, G);
+        w1 = __shfl_sync(mask, w[0], 1, G);
+    }
+    __device__ __forceinline__ uint64_t first() const { return w0; }
+    // the first lane of the group with pred set, -1 if none
+    __device__ __forceinline__ int first_lane(bool pred) const {
+        unsigned b = __ballot_sync(mask, pred) >> base;
+        if constexpr (G < 32) b &= (1u << G) - 1;
+        return b ? __ffs(b) - 1 : -1;
+    }
+    __device__ __forceinline__ void take(int f, int sg, uint32_t lc, int &sign, uint32_t &lcp) const {
+        sign = __shfl_sync(mask, sg, f, G);
+        lcp = __shfl_sync(mask, lc, f, G);
+    }
+};
+
+template <int G, int WPL>
+__device__ __forceinline__ uint64_t after_k0(const GroupRead<G, WPL> &P, uint32_t k) {
+    return (P.w0 << (2 * k)) | (P.w1 >> (64 - 2 * k));
+}
+
+// sign(P - t_s) and lcp, from word skip/32 on, G words per step
+template <int G, int WPL>
+__device__ __forceinline__ void gcompare_text(const uint64_t *__restrict__ text, uint64_t n, uint64_t s,
+                                              const GroupRead<G, WPL> &P, uint32_t m, uint32_t skip, int &sign,
+                                              uint32_t &lcp) {
+    const uint64_t slen = n - s;
+    const uint32_t nw = (m + 31) >> 5;
+    const uint32_t j0 = skip >> 5;
+    auto step = [&](int i, bool &done) {
+        const uint32_t j = P.lane + G * (uint32_t)i;
+        int sg = 0;
+        uint32_t lc = 0;
+        bool dec = false;
+        if (j >= j0 && j < nw) dec = cmp_text_word(text, s, slen, m, j, P.own(i), sg, lc);
+        const int f = P.first_lane(dec);
+        if (f >= 0) {
+            P.take(f, sg, lc, sign, lcp);
+            done = true;
+        }
+    };
+    bool done = false;
+    if constexpr (WPL > 0) {
+#pragma unroll
+        for (int i = 0; i < WPL; ++i) {
+            if (G * (uint32_t)(i + 1) <= j0) continue;
+            if (G * (uint32_t)i >= nw) break;
+            step(i, done);
+            if (done) return;
+        }
+    } else {
+        for (uint32_t i = j0 / G; G * i < nw; ++i) {
+            step((int)i, done);
+            if (done) return;
+        }
+    }
+    sign = 0;
+    lcp = m;
+}
+
+// the record compare of compare_rec: lane j < kWords takes cached word j (bases k+32j ..) against
+// P's bases k+32j .. (its own word and the next lane's)
+template <int G, int WPL, int L>
+__device__ __forceinline__ void gcompare_rec(const MatchArgs &a, const Rec<L> &r, const GroupRead<G, WPL> &P,
+                                             uint32_t m, uint32_t skip, int &sign, uint32_t &lcp, uint32_t &texts) {
+    const uint32_t k = a.k;
+    const uint64_t s = r.sa, len = a.n - s;
+    constexpr uint32_t CB = Rec<L>::kBases;
+    if (len < k || skip >= k + CB) {
+        ++texts;
+        gcompare_text(a.text, a.n, s, P, m, len < k ? 0u : skip, sign, lcp);
+        return;
+    }
+    const uint32_t avail = (uint32_t)((m < len ? (uint64_t)m : len) - k);
+    const uint64_t mine = P.own(0);
+    const uint64_t next = __shfl_down_sync(P.mask, mine, 1, G);
+    const uint32_t j = P.lane;
+    int sg = 0;
+    uint32_t lc = 0;
+    bool dec = false;
+    if (j < (uint32_t)Rec<L>::kWords && 32u * j < avail) {
+        const uint32_t b = 32u * j;
+        uint64_t c = r.c[0];
+#pragma unroll
+        for (int u = 1; u < Rec<L>::kWords; ++u)
+            if (j == (uint32_t)u) c = r.c[u];
+        const uint64_t msk = prefix_mask(min(min(32u, avail - b), CB - b));
+        const uint64_t x = ((mine << (2 * k)) | (next >> (64 - 2 * k))) & msk, y = c & msk;
+        if (x != y) {
+            dec = true;
+            lc = k + b + ((uint32_t)__clzll((long long)(x ^ y)) >> 1);
+            sg = x > y ? 1 : -1;
+        }
+    }
+    const int f = P.first_lane(dec);
+    if (f >= 0) {
+        P.take(f, sg, lc, sign, lcp);
+        return;
+    }
+    if (avail > CB) {
+        ++texts;
+        gcompare_text(a.text, a.n, s, P, m, k + CB, sign, lcp);
+        return;
+    }
+    if (m <= len) { sign = 0; lcp = m; }            // P is a prefix of the suffix (case 1)
+    else { sign = 1; lcp = (uint32_t)len; }          // the suffix is a proper prefix of P (reading A7)
+}
+
+template <int G, int WPL, int L>
+__device__ __forceinline__ void compare_probe(const MatchArgs &a, const Probe<L> &pr, const GroupRead<G, WPL> &P,
+                                              uint32_t m, uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp,
+                                              uint32_t &texts) {
+    if constexpr (L == L_PLAIN) {
+        ++texts;
+        gcompare_text(a.text, a.n, pr.s, P, m, skip, sign, lcp);
+    } else {
+        if (in_bracket) {
+            gcompare_rec(a, pr.r, P, m, skip, sign, lcp, texts);
+        } else {
+            ++texts;
+            gcompare_text(a.text, a.n, pr.r.sa, P, m, skip, sign, lcp);
+        }
+    }
+}
+
+template <int L, class RD>
+__device__ __forceinline__ void probe(const MatchArgs &a, const RD &P, uint32_t m, uint64_t p,
                                       uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts) {
     Probe<L> pr;
     pr.load(a, p);
-    compare_probe<QW, L>(a, pr, P, m, skip, in_bracket, sign, lcp, texts);
+    compare_probe(a, pr, P, m, skip, in_bracket, sign, lcp, texts);
 }
 
 // Binary search over (Lp1-1, R): LB rule (lower: R moves when P <= t) or RB rule (R moves when P < t).
-template <int QW, int L>
-__device__ __forceinline__ uint32_t bound(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint32_t Lp1,
+template <int L, class RD>
+__device__ __forceinline__ uint32_t bound(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1,
                                           uint32_t R, uint32_t lcpL, uint32_t lcpR, bool lower, bool in_bracket,
                                           uint32_t &steps, uint32_t &texts) {
     while (R > Lp1) {
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
-        probe<QW, L>(a, P, m, p, min(lcpL, lcpR), in_bracket, sign, lcp, texts);
+        probe<L>(a, P, m, p, min(lcpL, lcpR), in_bracket, sign, lcp, texts);
         ++steps;
         if (sign < 0 || (lower && sign == 0)) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
     }
@@ -304,8 +469,8 @@ __device__ __forceinline__ uint32_t bound(const MatchArgs &a, const QueryWords<Q
 }
 
 // One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.
-template <int QW, int L>
-__device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords<QW> &P, uint32_t m, uint32_t &lo,
+template <int L, class RD>
+__device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uint32_t m, uint32_t &lo,
                                             uint32_t &hi, uint32_t &steps, uint32_t &texts) {
     const uint32_t k = a.k;
     if (m == 0) {  // the empty read is a prefix of every suffix (reading A12)
@@ -319,8 +484,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
         const uint64_t x = P.first() >> (64 - 2 * m);
         const uint32_t Ta = ld_u32(a.table + (x << (2 * (k - m))));
         const uint32_t Tb = ld_u32(a.table + ((x + 1) << (2 * (k - m))));
-        lo = bound<QW, L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts);
-        hi = bound<QW, L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts);
+        lo = bound<L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts);
+        hi = bound<L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts);
         return;
     }
     // all suffixes before T[x] are < P, all from T[x+1] on are > P
@@ -335,7 +500,7 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
             const uint2 e = ld_v2u32(a.big_hash + h);
             if (e.x == (uint32_t)x) {
                 const uint32_t *T2 = a.big_sub + (uint64_t)e.y * 257;
-                const uint32_t y = (uint32_t)(read_after_k<QW>(P, k, 0) >> 56);  // bases k .. k+3
+                const uint32_t y = (uint32_t)(after_k0(P, k) >> 56);  // bases k .. k+3
                 Lp1 = ld_u32(T2 + y);
                 R = ld_u32(T2 + y + 1);
                 break;
@@ -350,7 +515,7 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
-        probe<QW, L>(a, P, m, p, min(lcpL, lcpR), true, sign, lcp, texts);
+        probe<L>(a, P, m, p, min(lcpL, lcpR), true, sign, lcp, texts);
         ++steps;
         if (sign == 0) {  // lo lies in (L, p], hi in (p, R]: the RB search starts from here
             split = true;
@@ -366,8 +531,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const QueryWords
     }
     // finish the LB search in (L, p], then the RB search in (p, R at the split].  (Interleaving the
     // two chains, both probes issued before either compare, measured 3% slower at C4: profiles/r01n.)
-    lo = bound<QW, L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts);
-    hi = bound<QW, L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts);
+    lo = bound<L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts);
+    hi = bound<L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts);
 }
 
 __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
@@ -401,11 +566,38 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
     if (m < a.min_len) {  // a partition cannot answer a read shorter than k (its window may leave the slice)
         lo = hi = 0xFFFFFFFFu;
     } else {
-        search_read<QW, L>(a, P, m, lo, hi, steps, texts);
+        search_read<L>(a, P, m, lo, hi, steps, texts);
     }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
     reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+}
+
+// Long reads (m > 128): G lanes per read slot (GroupRead), the same search as k_match.
+template <int G, int WPL, int L, bool STATS>
+__global__ void __launch_bounds__(256) k_match_group(const MatchArgs a) {
+    const uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    if (t >= a.Q) return;  // whole groups leave together
+    const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
+    const uint64_t row = a.rows_ordered ? t : q;
+    const uint32_t m = read_len(a, row);
+    GroupRead<G, WPL> P;
+    if (a.stride == 0) {
+        const uint64_t bit = 2ull * m * row;
+        P.init(a.words + (bit >> 6), (unsigned)(bit & 63), a.dense_words - (bit >> 6), (m + 31) >> 5);
+    } else {
+        P.init(a.words + row * a.stride, 0u, ~0ull, (m + 31) >> 5);
+    }
+    uint32_t lo, hi, steps = 0, texts = 0;
+    if (m < a.min_len) {
+        lo = hi = 0xFFFFFFFFu;
+    } else {
+        search_read<L>(a, P, m, lo, hi, steps, texts);
+    }
+    if (P.lane == 0) {
+        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+        if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+    }
 }
 
 }  // namespace sa_search

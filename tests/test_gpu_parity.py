@@ -205,6 +205,34 @@ def test_reads_of_129_to_256_bases(m_max):
         check_full(ref.tobytes(), words=words, lens=lens, layout=layout)
 
 
+@pytest.mark.parametrize("m_max", [256, 512, 1024, 2048, 3000])
+def test_group_kernel_hazards(m_max):
+    # strides > 4 words run the group-cooperative kernel (G = 8 / 16 / 32 lanes per read; 2 words per
+    # lane up to 2048 bases, words from memory beyond): the hazard batch (short reads, m < k, the empty
+    # read, text tails, reads running past the end) plus long exact, mutated and tail reads of up to m_max
+    rng = random.Random(m_max)
+    ref = synth.reference(synth.REF_REPEAT, 300_000, 71).tobytes().decode()
+    n = len(ref)
+    qs = hazard_queries(ref, 16, rng, extra=100)
+    for _ in range(300):
+        m = rng.randint(129, m_max)
+        i = rng.randrange(n - m + 1)
+        s = ref[i:i + m]
+        r = rng.random()
+        if r < 0.4:
+            qs.append(s)
+        elif r < 0.7:  # one substitution, anywhere (also past the 112 cached bases)
+            j = rng.randrange(m)
+            qs.append(s[:j] + "ACGT".replace(s[j], "")[rng.randrange(3)] + s[j + 1:])
+        elif r < 0.85:  # a text tail running past the end
+            qs.append(ref[n - rng.randint(1, m):] + "".join(rng.choice("ACGT") for _ in range(rng.randint(0, 40))))
+        else:
+            qs.append(ref[n - m:])  # the last m bases: a suffix exactly as long as the read
+    qs.append("A" * m_max)
+    for layout in LAYOUTS:
+        check_full(ref, qs, layout=layout)
+
+
 def test_stats_iteration_bound():
     # SA_MATCH_STATS: steps per boundary search never exceed ceil(log2(n+2)); joint lo+hi <= 2x
     ref = synth.reference(synth.REF_REPEAT, 1_000_000, 41)
