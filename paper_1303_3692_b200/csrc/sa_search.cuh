@@ -44,6 +44,7 @@ struct MatchArgs {
     const uint2 *__restrict__ big_hash; // SA_INDEX_SUBTABLE: {bucket, sub-table id}, empty = {~0, ~0}
     const uint32_t *__restrict__ big_sub;
     uint32_t big_bits;
+    bool out_at_slot;                   // SA_MATCH_STAGED_WRITE: slot t writes out[t] (the read is order[t])
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
         search_read<L>(a, P, m, lo, hi, steps, texts);
     }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
-    reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+    reinterpret_cast<uint2 *>(a.out)[a.out_at_slot ? t : q] = make_uint2(lo, hi);
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
 }
 
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(256) k_match_group(const MatchArgs a) {
         search_read<L>(a, P, m, lo, hi, steps, texts);
     }
     if (P.lane == 0) {
-        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+        reinterpret_cast<uint2 *>(a.out)[a.out_at_slot ? t : q] = make_uint2(lo, hi);
         if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
     }
 }

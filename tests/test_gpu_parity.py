@@ -274,6 +274,26 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     assert torch.equal(ow, w[perm.long()]) and torch.equal(ol, l[perm.long()])
     got2 = idx.match(ow, ol, order=perm, rows_ordered=True)
     assert torch.equal(got2, base)
+    # SA_MATCH_STAGED_WRITE: slot-order results written back through the partition pass
+    got3 = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda(), staged_write=True)
+    assert torch.equal(got3, base)
+    assert torch.equal(idx.match(w, l, presort=True, staged_write=True), base)
+    assert torch.equal(idx.match(ow, ol, order=perm, rows_ordered=True, staged_write=True), base)
+
+
+@pytest.mark.parametrize("Q", [1, 2, 3, 255, 256, 257, 70_001])
+def test_staged_write_sizes(Q):
+    # the partition pass on the read index's top 8 bits, for every small Q (1..8 index bits) and a ragged one
+    ref = synth.reference(synth.REF_REPEAT, 200_000, 53)
+    words, lens = synth.reads(ref, Q, 20, 100, 0.1, 0.05, 54)
+    idx = sa.Index(ref)
+    S = oracle.encode(ref)
+    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
+    w = torch.from_numpy(words.view(np.int64)).cuda()
+    l = torch.from_numpy(lens.view(np.int32)).cuda()
+    perm = idx.order(w, l)
+    got = idx.match(w, l, order=perm, staged_write=True).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, want)
 
 
 @pytest.mark.parametrize("m", [12, 31, 32, 100, 128, 150, 1000])
