@@ -24,10 +24,13 @@ $(PKG)/libsa.so: $(CU_SRCS) $(CU_HDRS)
 $(shell mkdir -p build)
 
 # A/B build variants (variants/*.so; bench.py / tests load one with SA_LIB_PATH=...)
-VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ldca.so
+VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ldca.so variants/libsa_l2_64.so \
+            variants/libsa_l2_64na.so
 variants/libsa_ldcg.so: DEFS := -DSA_LD_MODE=1
 variants/libsa_ldnoalloc.so: DEFS := -DSA_LD_MODE=2
 variants/libsa_ldca.so: DEFS := -DSA_LD_MODE=3
+variants/libsa_l2_64.so: DEFS := -DSA_LD_MODE=4
+variants/libsa_l2_64na.so: DEFS := -DSA_LD_MODE=5
 variants: $(VARIANTS)
 variants/%.so: $(CU_SRCS) $(CU_HDRS)
 	mkdir -p variants && $(NVCC) $(NVFLAGS) $(DEFS) -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_$(notdir $@).log || (cat build/ptxas_$(notdir $@).log; false)

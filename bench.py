@@ -68,8 +68,8 @@ def parse():
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
     ap.add_argument("--rows-ordered", action="store_true",
                     help="the ordering step also gathers the read rows into order (SA_MATCH_ROWS_ORDERED)")
-    ap.add_argument("--staged-write", action="store_true",
-                    help="SA_MATCH_STAGED_WRITE: slot-order results + partitioned write-back (include/sa.h)")
+    ap.add_argument("--cooperative", action="store_true",
+                    help="SA_MATCH_COOPERATIVE: reads over 128 bases searched by 8/16/32-lane groups")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -307,8 +307,7 @@ def main():
 
     stream = torch.cuda.current_stream()
     presort = not args.no_order
-    ws_flags = sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT | (sa.SA_MATCH_STAGED_WRITE if args.staged_write else 0)
-    ws = torch.empty(max(1, idx.workspace_size(Q, stride, ws_flags)),
+    ws = torch.empty(max(1, idx.workspace_size(Q, stride, sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT)),
                      dtype=torch.uint8, device=dev)
     perm = torch.empty(Q, dtype=torch.int32, device=dev) if presort else None
     rows_ordered = presort and args.rows_ordered
@@ -355,10 +354,10 @@ def main():
             tree.match(words, lens, fixed_len=fixed, out=out, stream=stream, order=perm)
         elif rows_ordered:
             idx.match(owords, olens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm, rows_ordered=True,
-                      staged_write=args.staged_write)
+                      cooperative=args.cooperative)
         else:
             idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm,
-                      staged_write=args.staged_write)
+                      cooperative=args.cooperative)
         if i is not None:
             ev[i][1].record(stream)
 
@@ -400,8 +399,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
             "clocks": sampler.result(),
-            "gpu_launches": args.steps * ((2 if presort else 1) + (1 if presort and args.staged_write else 0)),
-            "staged_write": bool(presort and args.staged_write),
+            "gpu_launches": args.steps * (2 if presort else 1),
             "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
                                           if presort else 0),
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},

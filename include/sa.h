@@ -99,13 +99,10 @@ typedef struct {
 #define SA_MATCH_ROWS_ORDERED 8u /* q_words / q_len are already in `order` order (sa_match_order's
                                     ordered_words / ordered_len): thread slot t reads row t and
                                     writes its interval to out_lohi at read order[t] */
-#define SA_MATCH_STAGED_WRITE 16u /* with an order (given or SA_MATCH_PRESORT): slot t writes its
-                                     interval to workspace slot t (coalesced), one radix pass
-                                     partitions (read, interval) by the read index's top 8 bits,
-                                     and a last kernel writes each partition's stretch of out_lohi
-                                     (L2-merged whole sectors instead of one read-modify-write per
-                                     scattered 8-byte result).  Same results; more workspace
-                                     (20*Q bytes + sort scratch).  Requires Q < 2^32. */
+#define SA_MATCH_COOPERATIVE 32u /* reads of more than 4 words (m > 128 bases) are searched by groups
+                                    of 8 / 16 / 32 lanes, one word per lane, compared with
+                                    __ballot_sync / __shfl_sync (the warp-cooperative compare of
+                                    north_star); default: one thread per read.  Same results. */
 
 /* Build the index of ref_ascii[0..n) (host memory, case-insensitive ACGT) on
  * the device: validate + pack to 2 bits/base, build the suffix array on the
@@ -142,7 +139,7 @@ sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
  *             (Alg. 1 lines 44-45, res[thd<<1] = LB, res[(thd<<1)+1] = RB, reading A8).
  *   workspace dev scratch of sa_match_workspace_size(..., flags, ...) bytes (may be NULL if
  *             that is 0).  With SA_MATCH_STATS its first 4*Q bytes receive the statistics.
- *   flags     0, or SA_MATCH_STATS / SA_MATCH_PRESORT / SA_MATCH_ROWS_ORDERED / SA_MATCH_STAGED_WRITE.
+ *   flags     0, or SA_MATCH_STATS / SA_MATCH_PRESORT / SA_MATCH_ROWS_ORDERED / SA_MATCH_COOPERATIVE.
  * Requirements: every length m <= 32*stride_words (longer lengths are clamped) and
  * m <= 65535; stride_words = 0 selects the dense layout (above).  Q == 0 is a no-op.
  * Errors: SA_EINVAL.  Asynchronous on `stream`. */

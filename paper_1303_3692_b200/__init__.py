@@ -26,7 +26,7 @@ SA_INDEX_REC32 = 2          # sa_index_opts.flags: 32-byte records caching 112 b
 SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windows << 16 into the workspace
 SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 12 bases before the search
 SA_MATCH_ROWS_ORDERED = 8   # sa_match_batch flags: rows already arranged in `order` order
-SA_MATCH_STAGED_WRITE = 16  # sa_match_batch flags: slot-order results, partitioned write-back to read order
+SA_MATCH_COOPERATIVE = 32   # sa_match_batch flags: reads over 128 bases searched by 8/16/32-lane groups
 SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 SA_INDEX_SUBTABLE = 8       # sa_index_opts.flags: (k+4)-base sub-tables for buckets of > 32 suffixes
 LAYOUTS = {"rec16": 0, "rec32": SA_INDEX_REC32, "plain": SA_INDEX_PLAIN}
@@ -244,7 +244,7 @@ class Index:
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
               presort: bool = False, workspace=None, order=None, rows_ordered: bool = False,
-              n_reads: Optional[int] = None, staged_write: bool = False):
+              n_reads: Optional[int] = None, cooperative: bool = False):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
@@ -253,7 +253,7 @@ class Index:
         order: optional CUDA int32 [Q] permutation from order() (thread slot t takes read order[t]).
         rows_ordered: words/lens are order()'s ordered_words/ordered_lens (row t is read order[t]).
         n_reads: with a 1-D `words` stream and fixed_len: the dense layout (include/sa.h).
-        staged_write: SA_MATCH_STAGED_WRITE (with an order or presort; include/sa.h).
+        cooperative: SA_MATCH_COOPERATIVE (reads over 128 bases: 8/16/32 lanes per read).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [Q] of steps | text windows << 16 (SA_MATCH_STATS).
@@ -269,9 +269,9 @@ class Index:
             out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
         flags = (SA_MATCH_STATS if want_stats else 0) | (SA_MATCH_PRESORT if presort else 0) | \
-                (SA_MATCH_ROWS_ORDERED if rows_ordered else 0) | (SA_MATCH_STAGED_WRITE if staged_write else 0)
+                (SA_MATCH_ROWS_ORDERED if rows_ordered else 0) | (SA_MATCH_COOPERATIVE if cooperative else 0)
         need = self.workspace_size(Q, stride, flags) \
-            if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_STAGED_WRITE) else 0
+            if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
         if need and (workspace is None or workspace.numel() < need):
             workspace = torch.empty(need, dtype=torch.uint8, device=words.device)
         _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),

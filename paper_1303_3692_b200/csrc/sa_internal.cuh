@@ -119,7 +119,9 @@ struct sa_index {
 
 // Loads of the search path.  SA_LD_MODE (compile time) selects the PTX cache operator for every
 // random access of the match kernel: 0 = ld.global.nc (read-only path, default), 1 = ld.global.cg
-// (L2 only), 2 = ld.global.nc.L1::no_allocate, 3 = ld.global.ca.
+// (L2 only), 2 = ld.global.nc.L1::no_allocate, 3 = ld.global.ca, 4 = ld.global.nc.L2::64B (64-byte
+// L2 fetch: 2 DRAM sectors per random access instead of 4, profiles/r01-2b/gather_async.txt),
+// 5 = 2 + 4.
 #ifndef SA_LD_MODE
 #define SA_LD_MODE 0
 #endif
@@ -129,6 +131,10 @@ struct sa_index {
 #define SA_LD_OP "ld.global.nc.L1::no_allocate"
 #elif SA_LD_MODE == 3
 #define SA_LD_OP "ld.global.ca"
+#elif SA_LD_MODE == 4
+#define SA_LD_OP "ld.global.nc.L2::64B"
+#elif SA_LD_MODE == 5
+#define SA_LD_OP "ld.global.nc.L1::no_allocate.L2::64B"
 #else
 #define SA_LD_OP "ld.global.nc"
 #endif

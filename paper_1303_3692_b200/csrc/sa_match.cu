@@ -97,23 +97,13 @@ __global__ void k_gather_rows(const uint64_t *__restrict__ words, const uint32_t
 
 struct PresortLayout {
     size_t stats = 0, keys_in = 0, keys_out = 0, perm_in = 0, perm_out = 0, cub = 0, cub_bytes = 0, total = 0;
-    // SA_MATCH_STAGED_WRITE: results in slot order, then partitioned by the read index's high bits
-    size_t slot_out = 0, part_keys = 0, part_vals = 0, part_cub = 0, part_cub_bytes = 0;
 };
-
-// bits of the read index the staged write partitions on: the top 8 of ceil(log2 Q)
-inline void staged_bits(uint64_t Q, int &begin_bit, int &end_bit) {
-    end_bit = 1;
-    while (end_bit < 32 && (1ull << end_bit) < Q) ++end_bit;
-    begin_bit = end_bit > 8 ? end_bit - 8 : 0;
-}
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // workspace of sa_match_order (order_only: the permutation goes to the caller's buffer) and of
 // sa_match_batch (stats first, then, with SA_MATCH_PRESORT, the same sort scratch + the permutation)
-sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, PresortLayout &L,
-                         bool staged = false) {
+sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, PresortLayout &L) {
     size_t off = 0;
     if (stats) { L.stats = off; off = align256(off + Q * 4); }
     if (presort) {
@@ -128,21 +118,6 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
         if (e != cudaSuccess) { sa_set_error("order size query: %s", cudaGetErrorString(e)); return SA_ECUDA; }
         L.cub = off;
         L.cub_bytes = b;
-        off = align256(off + b);
-    }
-    if (staged) {
-        if (Q >= (1ull << 32)) { sa_set_error("the staged write needs Q < 2^32"); return SA_EINVAL; }
-        L.slot_out = off; off = align256(off + Q * 8);
-        L.part_keys = off; off = align256(off + Q * 4);
-        L.part_vals = off; off = align256(off + Q * 8);
-        int bb, eb;
-        staged_bits(Q, bb, eb);
-        size_t b = 0;
-        cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr,
-                                                        (const uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)Q, bb, eb);
-        if (e != cudaSuccess) { sa_set_error("staged write size query: %s", cudaGetErrorString(e)); return SA_ECUDA; }
-        L.part_cub = off;
-        L.part_cub_bytes = b;
         off = align256(off + b);
     }
     L.total = off;
@@ -189,16 +164,6 @@ __global__ void k_scatter_results(const uint32_t *__restrict__ order, const uint
                                   uint2 *__restrict__ out) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (uint64_t)gridDim.x * blockDim.x)
         out[__ldg(order + t)] = in[t];
-}
-
-// SA_MATCH_STAGED_WRITE, last step: the (read, interval) pairs arrive partitioned by the read index's
-// top 8 bits, so the blocks running at any moment write into one or two ~Q/256-read stretches of out
-// (a few MB, L2-resident): L2 merges the 8-byte writes into whole sectors before they reach DRAM
-// instead of the read-modify-write one scattered 8-byte write costs.
-__global__ void k_unpartition(const uint32_t *__restrict__ q_of, const uint2 *__restrict__ v, uint64_t Q,
-                              uint2 *__restrict__ out) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += (uint64_t)gridDim.x * blockDim.x)
-        out[__ldg(q_of + i)] = v[i];
 }
 
 // ---- locate -----------------------------------------------------------------------------------
@@ -297,8 +262,7 @@ extern "C" sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, ui
     (void)stride_words;
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     PresortLayout L;
-    SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, flags & SA_MATCH_PRESORT, false, L,
-                          (flags & SA_MATCH_STAGED_WRITE) != 0));
+    SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, flags & SA_MATCH_PRESORT, false, L));
     *bytes = L.total;
     return SA_OK;
 }
@@ -348,10 +312,9 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                               uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *order,
-                              bool rows_ordered, cudaStream_t st, bool out_at_slot = false) {
+                              bool rows_ordered, cudaStream_t st, bool cooperative = false) {
     MatchArgs a;
     a.rows_ordered = rows_ordered;
-    a.out_at_slot = out_at_slot;
 
     a.text = idx->text;
     a.sa = idx->sa;
@@ -381,18 +344,19 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     }
     // one vector load per read row when the row is exactly QW words and suitably aligned
     const uintptr_t wp = reinterpret_cast<uintptr_t>(q_words);
-    a.vec_rows = (stride == 4 && (wp & 31) == 0) || (stride == 2 && (wp & 15) == 0);
+    // (stride a multiple of 4 beyond 4 words: the long-read path's 4-word chunks are single loads)
+    a.vec_rows = ((stride == 4 || (stride > 4 && stride % 4 == 0)) && (wp & 31) == 0) ||
+                 (stride == 2 && (wp & 15) == 0);
     a.dense_words = stride == 0 ? (Q * (uint64_t)fixed_len + 31) / 32 : 0;
     const bool st_on = stats != nullptr;
     const uint32_t nw = stride ? stride : (fixed_len + 31) / 32;  // register words needed
     cudaError_t e;
-    // reads of more than 4 words: G = 8 / 16 / 32 lanes per read (SA_MATCH_NO_GROUP=1: one thread per
-    // read, words from global memory -- the A/B baseline of DESIGN.md §7)
-    static const bool no_group = getenv("SA_MATCH_NO_GROUP") && atoi(getenv("SA_MATCH_NO_GROUP")) != 0;
+    // reads of more than 4 words: one thread per read, words from global memory; with
+    // SA_MATCH_COOPERATIVE G = 8 / 16 / 32 lanes per read (measured slower)
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
     else if (nw <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
     else if (nw <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
-    else if (no_group) e = launch_qw<0>(a, idx->layout, st_on, st);
+    else if (!cooperative) e = launch_qw<0>(a, idx->layout, st_on, st);
     else if (nw <= 8) e = launch_group<8, 1>(a, idx->layout, st_on, st);
     else if (nw <= 16) e = launch_group<16, 1>(a, idx->layout, st_on, st);
     else if (nw <= 32) e = launch_group<32, 1>(a, idx->layout, st_on, st);
@@ -408,16 +372,15 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
                                     void *stream) {
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
-    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED | SA_MATCH_STAGED_WRITE)) {
+    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED | SA_MATCH_COOPERATIVE)) {
         sa_set_error("unknown flags 0x%x", flags);
         return SA_EINVAL;
     }
     if (Q == 0) return SA_OK;
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     const bool presort = (flags & SA_MATCH_PRESORT) && !order;
-    const bool staged = (flags & SA_MATCH_STAGED_WRITE) && (order || presort);
     PresortLayout L;
-    SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, presort, false, L, staged));
+    SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, presort, false, L));
     if (L.total > 0 && (!workspace || ws_bytes < L.total)) {
         sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
         return SA_EINVAL;
@@ -435,25 +398,8 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         sa_set_error("SA_MATCH_ROWS_ORDERED needs the order the rows were arranged in");
         return SA_EINVAL;
     }
-    if (!staged)
-        return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st);
-    // staged write: slot t's interval to slot_out[t] (coalesced), partition (read, interval) by the read's
-    // top 8 index bits (one radix pass), then write each partition's stretch of out_lohi
-    uint64_t *slot_out = reinterpret_cast<uint64_t *>(ws + L.slot_out);
-    SA_TRY(match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, reinterpret_cast<uint32_t *>(slot_out), stats,
-                        order, rows_ordered, st, true));
-    int bb, eb;
-    staged_bits(Q, bb, eb);
-    uint32_t *pk = reinterpret_cast<uint32_t *>(ws + L.part_keys);
-    uint64_t *pv = reinterpret_cast<uint64_t *>(ws + L.part_vals);
-    size_t b = L.part_cub_bytes;
-    SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.part_cub, b, order, pk, slot_out, pv, (int64_t)Q, bb, eb, st));
-    uint64_t blocks = (Q + 255) / 256;
-    if (blocks > 148ull * 16) blocks = 148ull * 16;
-    k_unpartition<<<(unsigned)blocks, 256, 0, st>>>(pk, reinterpret_cast<const uint2 *>(pv), Q,
-                                                    reinterpret_cast<uint2 *>(out_lohi));
-    SA_CUDA_TRY(cudaGetLastError());
-    return SA_OK;
+    return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st,
+                        (flags & SA_MATCH_COOPERATIVE) != 0);
 }
 
 extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,

@@ -44,7 +44,6 @@ struct MatchArgs {
     const uint2 *__restrict__ big_hash; // SA_INDEX_SUBTABLE: {bucket, sub-table id}, empty = {~0, ~0}
     const uint32_t *__restrict__ big_sub;
     uint32_t big_bits;
-    bool out_at_slot;                   // SA_MATCH_STAGED_WRITE: slot t writes out[t] (the read is order[t])
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -89,27 +88,53 @@ struct QueryWords {
     __device__ __forceinline__ uint64_t first() const { return w[0]; }
     __device__ __forceinline__ uint64_t word(int j) const { return j < QW ? w[j] : 0ull; }
 };
+// Long reads: words 0..4 (the k-mer, the record-cached bases and the first text word) are kept in
+// registers; the rest is read from the row in 4-word chunks (one 256-bit load when the row is
+// 32-byte aligned and the stride a multiple of 4 words) as the text compare reaches it.
 template <>
 struct QueryWords<0> {
+    static constexpr int kHead = 5;
     const uint64_t *p;
     uint32_t nw;
     unsigned sh = 0;     // dense layout: bit shift of the read inside its first word
     uint64_t left = ~0ull;  // dense layout: words readable from p
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool) { p = q; nw = n; }
+    bool vec = false;    // chunk c = one 256-bit load at p + 4c
+    uint64_t h[kHead];   // words 0..4
+    __device__ __forceinline__ void fill_head() {
+#pragma unroll
+        for (int j = 0; j < kHead; ++j) h[j] = gword((uint32_t)j);
+    }
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool v) {
+        p = q;
+        nw = n;
+        vec = v;
+        fill_head();
+    }
     __device__ __forceinline__ void load_dense(const uint64_t *__restrict__ s, uint64_t bit, uint32_t n, uint64_t total) {
         p = s + (bit >> 6);
         sh = (unsigned)(bit & 63);
         nw = n;
         left = total - (bit >> 6);
+        fill_head();
     }
     __device__ __forceinline__ uint64_t raw(uint64_t j) const {
         return j < left ? ld_u64(p + j) : 0ull;
     }
-    __device__ __forceinline__ uint64_t word(int j) const {
-        if ((uint32_t)j >= nw) return 0ull;
+    __device__ __forceinline__ uint64_t gword(uint32_t j) const {
+        if (j >= nw) return 0ull;
         return sh ? (raw(j) << sh) | (raw(j + 1) >> (64 - sh)) : raw(j);
     }
-    __device__ __forceinline__ uint64_t first() const { return word(0); }
+    __device__ __forceinline__ uint64_t word(int j) const { return j < kHead ? h[j] : gword((uint32_t)j); }
+    // words 4c .. 4c+3 (0 past the read)
+    __device__ __forceinline__ void chunk(uint32_t c, uint64_t (&w)[4]) const {
+        if (vec && 4 * c + 3 < nw) {
+            ld_v4u64(p + 4 * c, w[0], w[1], w[2], w[3]);
+            return;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = gword(4 * c + u);
+    }
+    __device__ __forceinline__ uint64_t first() const { return h[0]; }
 };
 
 // ---- compare against the packed text --------------------------------------------------------
@@ -138,6 +163,48 @@ __device__ __forceinline__ bool cmp_text_word(const uint64_t *__restrict__ text,
     return false;
 }
 
+// cmp_text_word with the 32-base text window at s + 32j already loaded (tw)
+__device__ __forceinline__ bool cmp_word_window(uint64_t slen, uint32_t m, uint32_t j, uint64_t pw, uint64_t tw,
+                                                int &sign, uint32_t &lcp) {
+    const uint32_t base = j << 5;
+    const uint32_t plen = min(32u, m - base);
+    const uint64_t rem = slen > base ? slen - base : 0;
+    const uint32_t L = rem < plen ? (uint32_t)rem : plen;
+    if (L) {
+        const uint64_t mask = prefix_mask(L);
+        const uint64_t a = pw & mask, b = tw & mask;
+        if (a != b) {
+            lcp = base + ((uint32_t)__clzll((long long)(a ^ b)) >> 1);
+            sign = a > b ? 1 : -1;
+            return true;
+        }
+    }
+    if (L < plen) {
+        lcp = base + L;
+        sign = 1;
+        return true;
+    }
+    return false;
+}
+
+// four consecutive 32-base windows of the text from base b (b < n): text words w0 .. w0+4 from three
+// 16-byte loads (w0 <= ceil(n/32)-1, so the last word read is inside the zero guard words)
+__device__ __forceinline__ void text_windows4(const uint64_t *__restrict__ text, uint64_t b, uint64_t (&tw)[4]) {
+    const uint64_t w0 = b >> 5;
+    const uint64_t a = w0 & ~1ull;
+    uint64_t x[6];
+    ld_v2u64(text + a, x[0], x[1]);
+    ld_v2u64(text + a + 2, x[2], x[3]);
+    ld_v2u64(text + a + 4, x[4], x[5]);
+    const bool odd = (w0 & 1) != 0;
+    uint64_t r[5];
+#pragma unroll
+    for (int u = 0; u < 5; ++u) r[u] = odd ? x[u + 1] : x[u];
+    const unsigned sh = (unsigned)(b & 31u) << 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tw[u] = sh ? (r[u] << sh) | (r[u + 1] >> (64u - sh)) : r[u];
+}
+
 // sign(P - t_s), t_s = S[s .. min(s+m, n)), comparing from word skip/32 on; lcp = lcp(P, t_s).
 template <int QW>
 __device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, uint64_t n, uint64_t s,
@@ -154,8 +221,17 @@ __device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, 
             }
         }
     } else {
-        for (uint32_t j = j0; j < nw; ++j) {
-            if (cmp_text_word(text, s, slen, m, j, P.word((int)j), sign, lcp)) return;
+        // 4 words per step: the read chunk and four text windows are loaded together (vector loads),
+        // so a long verification is ~m/128 dependent round trips instead of ~m/32
+        for (uint32_t c = j0 >> 2; 4 * c < nw; ++c) {
+            uint64_t pw[4], tw[4] = {0, 0, 0, 0};
+            P.chunk(c, pw);
+            if (128ull * c < slen) text_windows4(text, s + 128ull * c, tw);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * c + u;
+                if (j >= j0 && j < nw && cmp_word_window(slen, m, j, pw[u], tw[u], sign, lcp)) return;
+            }
         }
     }
     sign = 0;
@@ -570,7 +646,7 @@ __global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
         search_read<L>(a, P, m, lo, hi, steps, texts);
     }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
-    reinterpret_cast<uint2 *>(a.out)[a.out_at_slot ? t : q] = make_uint2(lo, hi);
+    reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
 }
 
@@ -596,7 +672,7 @@ __global__ void __launch_bounds__(256) k_match_group(const MatchArgs a) {
         search_read<L>(a, P, m, lo, hi, steps, texts);
     }
     if (P.lane == 0) {
-        reinterpret_cast<uint2 *>(a.out)[a.out_at_slot ? t : q] = make_uint2(lo, hi);
+        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
         if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
     }
 }

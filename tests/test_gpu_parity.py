@@ -25,10 +25,10 @@ def _text(s):
     return s.encode("ascii") if isinstance(s, str) else s
 
 
-def gpu_match(idx, words, lens=None, fixed_len=None, presort=False, want_stats=False):
+def gpu_match(idx, words, lens=None, fixed_len=None, presort=False, want_stats=False, cooperative=False):
     w = torch.from_numpy(np.ascontiguousarray(words).view(np.int64)).cuda()
     l = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens).view(np.int32)).cuda()
-    res = idx.match(w, l, fixed_len=fixed_len, presort=presort, want_stats=want_stats)
+    res = idx.match(w, l, fixed_len=fixed_len, presort=presort, want_stats=want_stats, cooperative=cooperative)
     torch.cuda.synchronize()
     if want_stats:
         return res[0].cpu().numpy().view(np.uint32), res[1].cpu().numpy().view(np.uint32)
@@ -38,7 +38,8 @@ def gpu_match(idx, words, lens=None, fixed_len=None, presort=False, want_stats=F
 LAYOUTS = ["rec16", "rec32", "plain"]
 
 
-def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, layout="rec16", subtables=False):
+def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=True, layout="rec16", subtables=False,
+               cooperative=(False,)):
     """Build on the GPU; compare SA, table and every interval with the oracle."""
     S = oracle.encode(text_ascii)
     idx = sa.Index(text_ascii, k=k, layout=layout, subtables=subtables)
@@ -51,10 +52,11 @@ def check_full(text_ascii, queries=None, words=None, lens=None, k=0, check_sa=Tr
         words, lens = synth.pack_strings(queries)
     want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
     for presort in (False, True):
-        got = gpu_match(idx, words, lens, presort=presort)
-        bad = np.nonzero((got != want).any(axis=1))[0]
-        assert bad.size == 0, f"{bad.size} mismatches (layout={layout}, presort={presort}), first q={bad[0]}: " \
-                              f"got {got[bad[0]]} want {want[bad[0]]}"
+        for coop in cooperative:
+            got = gpu_match(idx, words, lens, presort=presort, cooperative=coop)
+            bad = np.nonzero((got != want).any(axis=1))[0]
+            assert bad.size == 0, f"{bad.size} mismatches (layout={layout}, presort={presort}, cooperative={coop}), " \
+                                  f"first q={bad[0]}: got {got[bad[0]]} want {want[bad[0]]}"
     return idx, S, sa_ref, got
 
 
@@ -193,7 +195,7 @@ def test_long_reads_generic_path():
     ref = synth.reference(synth.REF_REPEAT, 400_000, 21)
     for plain in LAYOUTS:  # the SA layout
         words, lens = synth.reads(ref, 3000, 150, 1000, 0.1, 0.2, 22)
-        check_full(ref.tobytes(), words=words, lens=lens, layout=plain)
+        check_full(ref.tobytes(), words=words, lens=lens, layout=plain, cooperative=(False, True))
 
 
 @pytest.mark.parametrize("m_max", [160, 256])
@@ -207,8 +209,8 @@ def test_reads_of_129_to_256_bases(m_max):
 
 @pytest.mark.parametrize("m_max", [256, 512, 1024, 2048, 3000])
 def test_group_kernel_hazards(m_max):
-    # strides > 4 words run the group-cooperative kernel (G = 8 / 16 / 32 lanes per read; 2 words per
-    # lane up to 2048 bases, words from memory beyond): the hazard batch (short reads, m < k, the empty
+    # strides > 4 words: the one-thread-per-read long-read path and SA_MATCH_COOPERATIVE's group kernel
+    # (G = 8 / 16 / 32 lanes per read; 2 words per lane up to 2048 bases, words from memory beyond): the hazard batch (short reads, m < k, the empty
     # read, text tails, reads running past the end) plus long exact, mutated and tail reads of up to m_max
     rng = random.Random(m_max)
     ref = synth.reference(synth.REF_REPEAT, 300_000, 71).tobytes().decode()
@@ -230,7 +232,7 @@ def test_group_kernel_hazards(m_max):
             qs.append(ref[n - m:])  # the last m bases: a suffix exactly as long as the read
     qs.append("A" * m_max)
     for layout in LAYOUTS:
-        check_full(ref, qs, layout=layout)
+        check_full(ref, qs, layout=layout, cooperative=(False, True))
 
 
 def test_stats_iteration_bound():
@@ -274,26 +276,6 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     assert torch.equal(ow, w[perm.long()]) and torch.equal(ol, l[perm.long()])
     got2 = idx.match(ow, ol, order=perm, rows_ordered=True)
     assert torch.equal(got2, base)
-    # SA_MATCH_STAGED_WRITE: slot-order results written back through the partition pass
-    got3 = idx.match(w, l, order=torch.from_numpy(order.view(np.int32)).cuda(), staged_write=True)
-    assert torch.equal(got3, base)
-    assert torch.equal(idx.match(w, l, presort=True, staged_write=True), base)
-    assert torch.equal(idx.match(ow, ol, order=perm, rows_ordered=True, staged_write=True), base)
-
-
-@pytest.mark.parametrize("Q", [1, 2, 3, 255, 256, 257, 70_001])
-def test_staged_write_sizes(Q):
-    # the partition pass on the read index's top 8 bits, for every small Q (1..8 index bits) and a ragged one
-    ref = synth.reference(synth.REF_REPEAT, 200_000, 53)
-    words, lens = synth.reads(ref, Q, 20, 100, 0.1, 0.05, 54)
-    idx = sa.Index(ref)
-    S = oracle.encode(ref)
-    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
-    w = torch.from_numpy(words.view(np.int64)).cuda()
-    l = torch.from_numpy(lens.view(np.int32)).cuda()
-    perm = idx.order(w, l)
-    got = idx.match(w, l, order=perm, staged_write=True).cpu().numpy().view(np.uint32)
-    assert np.array_equal(got, want)
 
 
 @pytest.mark.parametrize("m", [12, 31, 32, 100, 128, 150, 1000])
