@@ -486,6 +486,25 @@ def main():
             rg = sa.random_gather(local, buffer_bytes=16 << 30, access_bytes=32, n_threads=148 * 2048 * 2, loads=64)
             line["random_gather_32B"] = {"GBps": rg["GBps"], "Gsectors_per_s": rg["Gaccess_per_s"],
                                          "note": "independent random 32-B loads over 16 GiB"}
+            if "roofline" in line and "search_stats" in line:
+                # q/s ceiling = R_rand / random accesses per read.  A read's accesses: the
+                # read row (through the ordering), the bracket-table pair, one record per probe, one text
+                # window per window, the result store.  Each random access moves a 128-B DRAM line on this
+                # B200, so the line rate during k_match is compared with R_rand x 128 B.
+                ss = line["search_stats"]
+                apq = 3.0 + ss["mean_steps"] + ss["mean_text_windows"]
+                ceiling = rg["Gaccess_per_s"] * 1e9 / apq
+                kernel_qps = Q / avg_launch_s
+                rr = {"R_rand_Gaccess_per_s": rg["Gaccess_per_s"], "accesses_per_query": apq,
+                      "ceiling_queries_per_s": ceiling, "kernel_queries_per_s": kernel_qps,
+                      "frac": kernel_qps / ceiling,
+                      "note": "ceiling = every access an independent random access; frac > 1 is the line sharing "
+                              "the read ordering buys (neighbouring reads touch the same table / record lines); "
+                              "line_frac = DRAM line rate of k_match (ncu traffic) / (R_rand x 128 B)"}
+                if line["roofline"].get("traffic_GBps"):
+                    rr["dram_line_GBps"] = line["roofline"]["traffic_GBps"]
+                    rr["line_frac"] = line["roofline"]["traffic_GBps"] / (rg["Gaccess_per_s"] * 128.0)
+                line["random_access_roofline"] = rr
         except Exception as e:
             line["random_gather_32B"] = {"error": str(e)}
 

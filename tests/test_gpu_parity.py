@@ -278,6 +278,39 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     assert torch.equal(got2, base)
 
 
+def _stable_key_order(words, lens, kb):
+    key = (words[:, 0] >> np.uint64(64 - 2 * kb)).astype(np.uint64)
+    m = lens.astype(np.uint64)
+    short = m < kb
+    key[short] &= ~((np.uint64(1) << (np.uint64(2) * (np.uint64(kb) - m[short]))) - np.uint64(1))
+    return np.argsort(key, kind="stable").astype(np.uint32)
+
+
+_ORDER_INDEX = []
+
+
+@pytest.mark.parametrize("Q", [1, 31, 65536 * 3 + 17])
+@pytest.mark.parametrize("skew", ["random", "one_key", "few_keys"])
+@pytest.mark.parametrize("key_bases", [1, 4, 7, 10, 12, 13, 16])
+def test_order_equals_stable_argsort(Q, skew, key_bases):
+    """sa_match_order = the stable sort of the reads by their first key_bases bases, bit-exact: random,
+    one-key and few-key batches, reads shorter than the key (masked), Q across sort-tile sizes."""
+    if not _ORDER_INDEX:
+        _ORDER_INDEX.append(sa.Index(synth.reference(synth.REF_UNIFORM, 100_000, 71)))
+    idx = _ORDER_INDEX[0]
+    rng = np.random.default_rng(72 + Q + key_bases)
+    words = rng.integers(0, 2**63, size=(Q, 2), dtype=np.int64).view(np.uint64)
+    if skew == "one_key":
+        words[:, 0] = np.uint64(0x1B1B1B1B1B1B1B1B)
+    elif skew == "few_keys":
+        words[:, 0] = np.array([0, 0xFFFFFFFFFFFFFFFF, 0x5555555555555555], dtype=np.uint64)[rng.integers(0, 3, Q)]
+    lens = rng.integers(0, 65, size=Q).astype(np.uint32)
+    w = torch.from_numpy(words.view(np.int64)).cuda()
+    l = torch.from_numpy(lens.view(np.int32)).cuda()
+    got = idx.order(w, l, key_bases=key_bases).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, _stable_key_order(words, lens, key_bases))
+
+
 @pytest.mark.parametrize("m", [12, 31, 32, 100, 128, 150, 1000])
 def test_dense_layout_matches_strided(m):
     ref = synth.reference(synth.REF_REPEAT, 1_000_000, 61)
