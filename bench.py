@@ -562,6 +562,12 @@ def main():
                 raise RuntimeError("dense-layout device path disagrees with the strided path")
             line["e2e"]["split_ms"] = {"input": ev3[0].elapsed_time(ev3[1]), "kernel": ev3[1].elapsed_time(ev3[2]),
                                        "output": ev3[2].elapsed_time(ev3[3])}
+            # the bound of the end-to-end path: the host->device copy of the reads alone
+            sp = line["e2e"]["split_ms"]
+            h2d_rate = Q * world / (sp["input"] * 1e-3)
+            line["e2e"]["bound"] = {"kind": "pcie_h2d", "h2d_GBps": h2d / (sp["input"] * 1e-3) / 1e9,
+                                    "h2d_only_queries_per_s": h2d_rate,
+                                    "frac": line["e2e"]["value"] / h2d_rate}
             del dwd, outd, permd
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----

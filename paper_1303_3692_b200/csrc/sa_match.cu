@@ -17,7 +17,7 @@ using sa_search::MatchArgs;
 
 template <int QW, int L, bool STATS>
 cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
-    const int threads = 256;
+    const int threads = SA_MATCH_THREADS;
     const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
     sa_search::k_match<QW, L, STATS><<<blocks, threads, 0, st>>>(a);
     return cudaGetLastError();

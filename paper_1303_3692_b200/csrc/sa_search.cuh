@@ -630,8 +630,16 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 // profiles/r01b, r01c: it de-correlates the lanes' addresses), and a software-pipelined variant that
 // prefetches the next read's row during the current search (profiles/r01t: 2% slower -- the kernel is
 // bound by DRAM line throughput, not by the latency of the chain's head).
+#ifndef SA_MATCH_THREADS
+#define SA_MATCH_THREADS 256  // block size of k_match (A/B builds: variants/)
+#endif
+#ifdef SA_MATCH_MINB  // minimum resident blocks per SM requested from ptxas (a register cap)
+#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS, SA_MATCH_MINB)
+#else
+#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS)
+#endif
 template <int QW, int L, bool STATS>
-__global__ void __launch_bounds__(256) k_match(const MatchArgs a) {
+__global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.Q) return;
     const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;  // the read; its result goes to out[q]
