@@ -654,7 +654,12 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
         search_read<L>(a, P, m, lo, hi, steps, texts);
     }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
+#ifdef SA_OUT_PAD  // experiment: one full 32-byte sector per read (no ECC read-modify-write of a partial sector)
+    reinterpret_cast<uint4 *>(a.out)[2 * q] = make_uint4(lo, hi, 0u, 0u);
+    reinterpret_cast<uint4 *>(a.out)[2 * q + 1] = make_uint4(0u, 0u, 0u, 0u);
+#else
     reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+#endif
     if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
 }
 
