@@ -91,9 +91,12 @@ struct QueryWords {
 // Long reads: words 0..4 (the k-mer, the record-cached bases and the first text word) are kept in
 // registers; the rest is read from the row in 4-word chunks (one 256-bit load when the row is
 // 32-byte aligned and the stride a multiple of 4 words) as the text compare reaches it.
+#ifndef SA_QW0_HEAD
+#define SA_QW0_HEAD 5  // words of a long read kept in registers (A/B builds: variants/)
+#endif
 template <>
 struct QueryWords<0> {
-    static constexpr int kHead = 5;
+    static constexpr int kHead = SA_QW0_HEAD;
     const uint64_t *p;
     uint32_t nw;
     unsigned sh = 0;     // dense layout: bit shift of the read inside its first word
@@ -221,6 +224,14 @@ __device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, 
             }
         }
     } else {
+        if (nw <= j0 + 2) {  // one or two words left (e.g. bases 128..149 of a 150-base read past rec32's
+                             // cache): word by word, no 4-window load (profiles/r01-3/l_*: 10% at m = 150)
+            for (uint32_t j = j0; j < nw; ++j)  // (gword: the row word from L1, not a dynamic index into h)
+                if (cmp_text_word(text, s, slen, m, j, P.gword(j), sign, lcp)) return;
+            sign = 0;
+            lcp = m;
+            return;
+        }
         // 4 words per step: the read chunk and four text windows are loaded together (vector loads),
         // so a long verification is ~m/128 dependent round trips instead of ~m/32
         for (uint32_t c = j0 >> 2; 4 * c < nw; ++c) {
