@@ -224,6 +224,11 @@ class Index:
         _check(lib().sa_match_workspace_size(self._h, Q, stride, flags, ctypes.byref(ws)), "sa_match_workspace_size")
         return ws.value
 
+    def order_workspace_size(self, Q: int) -> int:
+        ws = _sz()
+        _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(ws)), "sa_match_order_workspace_size")
+        return ws.value
+
     def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None,
               key_bases: int = 0, ordered_words=None, ordered_lens=None, n_reads: Optional[int] = None):
         """sa_match_order: a permutation of the reads sorted by their first key_bases bases (0 = 12);
