@@ -18,8 +18,15 @@ synth/libsynth.so: synth/synth.c
 oracle/liboracle.so: oracle/oracle.c
 	$(CC) $(CFLAGS) -shared -o $@ $<
 
-$(PKG)/libsa.so: $(CU_SRCS) $(CU_HDRS)
-	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas.log || (cat build/ptxas.log; false)
+# one object per translation unit (make -j compiles them in parallel), then one shared library
+CU_OBJS   := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
+
+build/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $< 2> build/ptxas_$*.log || (cat build/ptxas_$*.log; false)
+
+$(PKG)/libsa.so: $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcudart
+	cat build/ptxas_sa_*.log > build/ptxas.log
 
 $(shell mkdir -p build)
 

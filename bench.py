@@ -4,11 +4,15 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...          (one rank per GPU, NCCL)
 
-A step is one pass of the hot path -- ``sa_match_batch`` over this rank's whole batch of packed
-reads (bracket lookup, joint lo/hi binary search, interval write) -- with the index and the reads
-already resident in HBM.  The index build is off the timed path.
-Multi-GPU: the index is replicated, every rank matches its own fixed-size shard of reads (weak
-scaling, no data-path collective); elapsed time is the max over ranks (NCCL all_reduce MAX).
+A step is one pass of the hot path -- ``sa_match_order`` + ``sa_match_batch`` over this rank's whole
+batch of packed reads (read ordering, bracket lookup, joint lo/hi binary search, interval write) --
+with the index and the reads already resident in HBM.  The index build is off the timed path
+(SURVEY.md Sec. 8(a) a1-a3).
+Multi-GPU: the index is replicated and the job's Q reads are cut into N
+contiguous slices, one per rank (strong scaling: C4 is "100M reads sharded over 1/2/4/8 GPUs";
+``--weak`` gives every rank its own Q reads instead); no data-path collective; elapsed time is the
+max over ranks (all_reduce MAX).  ``--gpus N`` without torchrun (WORLD_SIZE unset) starts the N
+ranks itself.
 
 `--impl reference` times the CPU oracle (oracle/: the streaming counting oracle, no suffix array)
 on a bounded sample of the same workload on this box's host cores.
@@ -19,7 +23,9 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -47,7 +53,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4", choices=sorted(synth.CONFIGS))
     ap.add_argument("--m", type=int, default=None, help="C5 read length (16..1000)")
-    ap.add_argument("--q", type=int, default=None, help="override reads per GPU")
+    ap.add_argument("--q", type=int, default=None, help="override the job's reads Q (split over the ranks)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank matches its own Q reads (default: the Q reads are split over the ranks)")
     ap.add_argument("--k", type=int, default=0, help="k-mer bracket k (0 = auto: floor(log4 n)+1, <= 16)")
     ap.add_argument("--layout", default="rec32", choices=["rec16", "rec32", "plain"],
                     help="SA layout: 16-byte records caching 48 bases (default), 32-byte records caching 112 "
@@ -76,7 +84,9 @@ def parse():
     ap.add_argument("--no-locate", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to test the multi-rank path with ranks sharing a GPU)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the cpu_baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU time of the cpu_baseline's single-thread sample (and of the reference arm's step)")
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000, help="cpu_baseline: at most this many reads")
     return ap.parse_args()
 
 
@@ -90,12 +100,20 @@ def workload(args):
     return cfg
 
 
-def config_json(cfg, world, k=None):
-    d = {"workload": f"{cfg.name}: {cfg.description}", "n_bases": cfg.n, "reads_per_gpu": cfg.Q,
-         "global_reads": cfg.Q * world, "read_len": (cfg.m_min if cfg.m_min == cfg.m_max else [cfg.m_min, cfg.m_max]),
-         "parallelism": f"replicated index x{world}, read shards (no data-path collective)",
-         "l2": "inputs larger than L2 (index + reads >> 126 MB); no flush" if cfg.n * 4 > 2 ** 30 else
-               "index fits L2 (L2-resident workload); no flush"}
+def config_json(cfg, world, reads_per_gpu, weak=False, k=None, index_bytes=None):
+    d = {"workload": f"{cfg.name}: {cfg.description}", "n_bases": cfg.n, "reads_per_gpu": reads_per_gpu,
+         "global_reads": reads_per_gpu * world if weak else cfg.Q,
+         "read_len": (cfg.m_min if cfg.m_min == cfg.m_max else [cfg.m_min, cfg.m_max]),
+         "parallelism": f"replicated index x{world}, " + (f"{cfg.Q} reads per rank (weak)" if weak else
+                                                           f"{cfg.Q} reads split in {world} contiguous shards") +
+                        " (no data-path collective)"}
+    if index_bytes is not None:
+        # what one step reads at random vs the 126 MB L2 (inputs larger than L2 need no flush)
+        resident = index_bytes + reads_per_gpu * cfg.stride * 8
+        d["l2"] = (f"inputs larger than L2 (index {index_bytes / 1e9:.2f} GB + reads >> 126 MB); no flush"
+                   if index_bytes > 126e6 else
+                   f"index fits L2 ({index_bytes / 1e6:.1f} MB <= 126 MB: an L2-resident workload); no flush")
+        d["resident_bytes"] = resident
     if k is not None:
         d["kmer_k"] = k
     return d
@@ -159,37 +177,77 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def algorithmic_bytes_per_query(layout, m, probes, text_windows):
-    """sector-granular bytes of the accesses the search itself makes per read.
-
-    Every random access moves one 32-B sector: the bracket-table pair (1), one record / SA entry per
-    probe, one per text window (plain: every probe; rec16: the bases past the 48 cached ones), the
-    read row (32 B, gathered through the ordering; ceil(m/4) B beyond 128 bases) and the 8-B result.
-    `probes` and `text_windows` are the per-read means counted by the SA_MATCH_STATS launch on this
-    very batch, so the figure is the algorithm's own access count on the workload, not a cache model."""
-    read = max(32.0, math.ceil(m / 4.0))
-    return 32.0 + 32.0 * probes + 32.0 * text_windows + read + 8.0
+def sector_bytes_per_query(m, probes, text_windows):
+    """The 32-B-sector access model of r01 (kept for continuity): bracket pair + one sector per probe and
+    per text window + the read row + the 8-B result."""
+    return 32.0 + 32.0 * probes + 32.0 * text_windows + max(32.0, math.ceil(m / 4.0)) + 8.0
 
 
-def traffic_per_launch(workload_name):
-    """dram bytes (read + write) per k_match launch from the committed ncu --set full summary, if any."""
+def traffic_entry(key):
+    """DRAM bytes per read (read + write) of k_match from the committed ncu --set full capture of this exact
+    configuration (profiles/traffic.json, written from the profile of the same commit), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        return t.get(workload_name)
+        e = t.get(key)
+        return e if isinstance(e, dict) else None
     except Exception:
         return None
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def free_port():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args):
+    """`--gpus N` without torchrun: start N ranks of this script (RANK / WORLD_SIZE / LOCAL_RANK /
+    MASTER_* set as torchrun would, rendezvous on 127.0.0.1).  Rank 0 prints the JSON line.  If a rank
+    fails, the others are stopped (by their own process handles) and its exit code is returned."""
+    port = free_port()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(args.gpus), LOCAL_RANK=str(r),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rc = 0
+    live = list(procs)
+    while live:
+        for p in list(live):
+            code = p.poll()
+            if code is None:
+                continue
+            live.remove(p)
+            if code != 0 and rc == 0:
+                rc = code
+                for q in live:
+                    q.terminate()
+        time.sleep(0.2)
+    return rc
+
+
 # ---------------------------------------------------------------------------------------------
 def run_reference_arm(args):
-    """The CPU oracle on this box's host cores (rank 0 only)."""
+    """The CPU oracle on this box's host cores (rank 0 only; it never loads libsa)."""
     import oracle
+    from paper_1303_3692_b200 import shard
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = workload(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     t0 = time.time()
     ref = cfg.reference()
     S = oracle.encode(ref)
@@ -210,8 +268,8 @@ def run_reference_arm(args):
     v = s * len(times) / tot
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": config_json(cfg, world),
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": config_json(cfg, world, shard.shard(0, world, cfg.Q, weak=args.weak)[1], weak=args.weak),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{s} reads per step of the {cfg.name} read stream, streaming counting "
                                        f"oracle over all {cfg.n} suffixes (no suffix array)"},
@@ -230,18 +288,43 @@ def sample_size(cfg, cores, seconds):
     return max(16, min(s, cfg.Q))
 
 
-def cpu_baseline(cfg, ref, seconds):
+def cpu_baseline(cfg, ref, idx, words, lens, got, seconds, max_sample):
+    """SURVEY.md §8(d) / BASELINE.md "CPU-baseline plan": the oracle's textbook lower/upper-bound search
+    (oracle_search_batch, P:L173-230 corrected) over the GPU-built suffix array, passed as data, on a
+    sample of this run's reads, single-threaded and on all host cores; rates extrapolated to the batch.
+    The sample's intervals are also compared with the GPU's (`agrees_with_gpu`)."""
     import oracle
     S = oracle.encode(ref)
+    t0 = time.perf_counter()
+    sa_host = idx.export_sa()
+    export_s = time.perf_counter() - t0
     cores = oracle.max_threads()
-    s = sample_size(cfg, cores, seconds)
-    words, lens = cfg.reads(ref, q_count=s)
+    Q = words.shape[0]
+    lw = None if lens is None else lens
+    # calibrate the single-thread rate on a small prefix, then size the sample to ~`seconds`
+    c = min(Q, 2000)
     t = time.perf_counter()
-    oracle.count_batch(S, words, lens)
-    dt = time.perf_counter() - t
-    return {"value": s / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "seconds": dt,
-            "sample": f"first {s} reads of the {cfg.name} read stream, streaming counting oracle over all "
-                      f"{cfg.n} suffixes (no suffix array), {cores} threads"}
+    oracle.search_batch(S, sa_host, words[:c], None if lw is None else lw[:c], fixed_len=cfg.m_max, nthreads=1)
+    per = max(1e-9, (time.perf_counter() - t) / c)
+    s1 = int(max(c, min(max_sample, Q, seconds / per)))
+    t = time.perf_counter()
+    r1 = oracle.search_batch(S, sa_host, words[:s1], None if lw is None else lw[:s1], fixed_len=cfg.m_max, nthreads=1)
+    d1 = time.perf_counter() - t
+    sa_ = min(max_sample, Q)
+    t = time.perf_counter()
+    ra = oracle.search_batch(S, sa_host, words[:sa_], None if lw is None else lw[:sa_], fixed_len=cfg.m_max, nthreads=0)
+    da = time.perf_counter() - t
+    agree = bool(np.array_equal(ra.astype(np.uint32), got[:sa_]) and np.array_equal(r1.astype(np.uint32), got[:s1]))
+    v1, va = s1 / d1, sa_ / da
+    return {"value": va, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"first {sa_} reads of this run's {cfg.name} batch (all cores) / first {s1} (1 thread): "
+                      f"textbook lower/upper-bound binary search (oracle_search_batch) over the GPU-built suffix "
+                      f"array passed as data ({cfg.n} suffixes); rates extrapolated to the batch",
+            "extrapolated": True,
+            "single_thread": {"value": v1, "sample_reads": s1, "seconds": d1},
+            "all_cores": {"value": va, "sample_reads": sa_, "seconds": da, "threads": cores},
+            "projected_seconds_full_batch": {"1_thread": Q / v1, "all_cores": Q / va},
+            "sa_export_seconds": export_s, "agrees_with_gpu": agree}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -250,6 +333,8 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     import torch
     import torch.distributed as dist
     import paper_1303_3692_b200 as sa
@@ -259,13 +344,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        log(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without torchrun to let bench.py start the ranks")
     ndev = torch.cuda.device_count()
     if local >= ndev:  # test mode only (--dist-backend gloo): several ranks share the visible GPUs
         if args.dist_backend == "nccl":
             raise RuntimeError(f"LOCAL_RANK {local} but only {ndev} GPUs visible")
         local = local % ndev
     torch.cuda.set_device(local)
+    numa = shard.bind_numa_local(local)  # before any pinned host buffer is allocated and touched
     if world > 1:
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -291,13 +378,12 @@ def main():
         tree = sa.Tree(idx)
         log(f"flattened suffix tree: {tree.nodes} nodes, {tree.device_bytes / 1e9:.2f} GB, {time.time() - t1:.1f}s")
     t0 = time.time()
-    Q = cfg.Q
+    q_begin, Q = shard.shard(rank, world, cfg.Q, weak=args.weak)  # this rank's contiguous slice of the reads
     stride = cfg.stride
     fixed = cfg.m_max if cfg.m_min == cfg.m_max else None
     words_h = torch.empty((Q, stride), dtype=torch.int64, pin_memory=True)
     lens_h = torch.empty(Q, dtype=torch.int32, pin_memory=True)
-    q_begin, _ = shard.shard(rank, world, Q)
-    cfg.reads(ref, q_begin=q_begin, words_out=words_h.numpy().view(np.uint64),
+    cfg.reads(ref, q_begin=q_begin, q_count=Q, words_out=words_h.numpy().view(np.uint64),
               lens_out=lens_h.numpy().view(np.uint32))
     words = words_h.to(dev, non_blocking=True)
     lens = None if fixed else lens_h.to(dev, non_blocking=True)
@@ -386,18 +472,22 @@ def main():
     # per-shard summary gathered over NCCL (the only collective): hits, sum of counts, checksum
     summary_all = shard.gather_summaries(shard.summarize(out))
 
-    total_reads = Q * world * args.steps
+    global_reads = shard.all_reduce_sum(Q, dev)  # the reads all ranks matched per step
+    total_reads = global_reads * args.steps
     value = total_reads / (elapsed_ms * 1e-3)
     ms_per_step = elapsed_ms / args.steps
 
     m_alg = cfg.m_max if fixed else (cfg.m_min + cfg.m_max) / 2
     avg_launch_s = statistics.mean(launch_ms) * 1e-3
     peak, peak_src = measured_peaks()
-    traffic = traffic_per_launch(f"{cfg.name}/{args.layout}")
+    traffic_key = f"{cfg.name}/{args.layout}/k{idx.k}/Q{Q}" + ("/tree" if args.tree else "")
+    traffic_e = traffic_entry(traffic_key)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": config_json(cfg, world, idx.k),
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": config_json(cfg, world, Q, weak=args.weak, k=idx.k, index_bytes=idx.device_bytes),
+            "numa": numa,
             "clocks": sampler.result(),
             "gpu_launches": args.steps * (2 if presort else 1),
             "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
@@ -427,26 +517,43 @@ def main():
         torch.cuda.synchronize()
         if not torch.equal(chk, out):
             raise RuntimeError("instrumented launch disagrees with the timed launches")
-        stv = st.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        stv = st[0].to(torch.int64) & 0xFFFFFFFF
+        ubytes = (st[1].to(torch.int64) & 0xFFFFFFFF).double()
         steps_t, texts_t = (stv & 0xFFFF).double(), (stv >> 16).double()
         line["search_stats"] = {"mean_steps": float(steps_t.mean()), "mean_text_windows": float(texts_t.mean()),
                                 "p99_steps": float(torch.quantile(steps_t[:1 << 20], 0.99)),
-                                "max_steps": float(steps_t.max())}
+                                "max_steps": float(steps_t.max()),
+                                "mean_algorithmic_bytes": float(ubytes.mean())}
 
         # ---- roofline of the dominant kernel (k_match; the ordering sort is CUB's) ----
-        bpq = algorithmic_bytes_per_query(args.layout, m_alg, line["search_stats"]["mean_steps"],
-                                          line["search_stats"]["mean_text_windows"])
+        # achieved = SURVEY.md §8(d)'s useful bytes, counted per read by the instrumented launch of this very
+        # batch (SA_MATCH_STATS), x Q / the mean k_match launch time of the timed steps.
+        bpq = line["search_stats"]["mean_algorithmic_bytes"]
         if tree is not None:
             line["search_stats"]["note"] = "counts of the SA search (the timed kernel is the tree walk)"
         achieved = bpq * Q / avg_launch_s / 1e9
+        traffic = traffic_e["dram_bytes_per_read"] * Q if traffic_e else None
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "kernel": "k_tree_match" if tree is not None else "k_match",
-                    "algorithmic_bytes_per_query": bpq, "peak_source": peak_src}
+                    "algorithmic_bytes_per_query": bpq,
+                    "algorithmic_bytes_formula": "SURVEY.md 8(d): ceil(m/4) read + 8 table pair + sum over probes of "
+                                                 "(4 B SA entry + ceil(decided bases/4)) + 8 result, decided bases = "
+                                                 "from min(lcp_L, lcp_R) to the first difference (all m at a match); "
+                                                 "per read from SA_MATCH_STATS on this batch",
+                    "measured_counts": {"probes_per_query": line["search_stats"]["mean_steps"],
+                                        "text_windows_per_query": line["search_stats"]["mean_text_windows"]},
+                    "sector_bytes_per_query": sector_bytes_per_query(m_alg, line["search_stats"]["mean_steps"],
+                                                                     line["search_stats"]["mean_text_windows"]),
+                    "peak_source": peak_src, "launch_ms_mean": avg_launch_s * 1e3}
         if tree is not None:
-            roofline["note"] = "bytes model of the SA search; the tree walk moves one 32-B node + one text window per level"
-        if traffic:
+            roofline["note"] = "bytes of the SA search; the tree walk moves one 32-B node + one text window per level"
+        if traffic_e:
+            roofline["traffic_source"] = traffic_e.get("source")
+            roofline["traffic_bytes_per_query"] = traffic_e["dram_bytes_per_read"]
             roofline["traffic_GBps"] = traffic / avg_launch_s / 1e9
             roofline["traffic_frac"] = roofline["traffic_GBps"] / peak
+        else:
+            roofline["traffic_source"] = f"no committed ncu capture for {traffic_key} (profiles/traffic.json)"
         line["roofline"] = roofline
         del st, chk
 
@@ -480,12 +587,19 @@ def main():
                           "gather_GBps": npos * 4 * 2 / max(1e-9, l1b.elapsed_time(l2) * 1e-3) / 1e9}
         del offs, pos
 
-    # ---- random-gather microbenchmark (context for the roofline; untimed) ----
+    # ---- random-gather microbenchmark (the random-access roofline's denominator; untimed) ----
+    # R_rand = the best of the load forms the microbenchmark offers (plain, .nc, .nc.L1::no_allocate) for
+    # independent random 32-B loads over 16 GiB, measured in this run.
     if rank == 0:
         try:
-            rg = sa.random_gather(local, buffer_bytes=16 << 30, access_bytes=32, n_threads=148 * 2048 * 2, loads=64)
-            line["random_gather_32B"] = {"GBps": rg["GBps"], "Gsectors_per_s": rg["Gaccess_per_s"],
-                                         "note": "independent random 32-B loads over 16 GiB"}
+            modes = {"ld": 0, "ld.global.nc": 10, "ld.global.nc.L1::no_allocate": 13}
+            rgs = {name: sa.random_gather(local, buffer_bytes=16 << 30, access_bytes=32, n_threads=148 * 2048 * 2,
+                                          loads=64, dependent=mode) for name, mode in modes.items()}
+            best = max(rgs, key=lambda k_: rgs[k_]["Gaccess_per_s"])
+            rg = rgs[best]
+            line["random_gather_32B"] = {"GBps": rg["GBps"], "Gsectors_per_s": rg["Gaccess_per_s"], "best_mode": best,
+                                         "by_mode_Gaccess_per_s": {k_: v["Gaccess_per_s"] for k_, v in rgs.items()},
+                                         "note": "independent random 32-B loads over 16 GiB, 606k threads x 64"}
             if "roofline" in line and "search_stats" in line:
                 # q/s ceiling = R_rand / random accesses per read.  A read's accesses: the
                 # read row (through the ordering), the bracket-table pair, one record per probe, one text
@@ -516,7 +630,7 @@ def main():
         if dense:
             nwords = Q // 32 * cfg.m_max
             dw = torch.empty(nwords, dtype=torch.int64, pin_memory=True)
-            cfg.reads(ref, q_begin=q_begin, words_out=dw.numpy().view(np.uint64), dense=True)
+            cfg.reads(ref, q_begin=q_begin, q_count=Q, words_out=dw.numpy().view(np.uint64), dense=True)
             wn, ln, h2d = dw.numpy(), None, nwords * 8
         else:
             wn, ln = words_h.numpy(), (None if fixed else lens_h.numpy())
@@ -535,10 +649,10 @@ def main():
         dt = shard.max_over_ranks(dt, dev)
         if not np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32)):
             raise RuntimeError("host-buffer path disagrees with the device path")
-        line["e2e"] = {"value": Q * world * e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        line["e2e"] = {"value": global_reads * e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": Q * 8, "steps": e2e_steps,
                        "layout": "dense 2-bit stream" if dense else f"{stride} words per read",
-                       "path": "sa_match_batch_host (pinned host buffers, 2 streams, 4M-read chunks)",
+                       "path": "sa_match_batch_host (pinned host buffers, 2 streams, 4M-read chunks, each ordered)",
                        "overlapped_ms_per_step": dt * 1e3 / e2e_steps}
         # the paper's Table V split (input / kernel / output time), measured one phase at a
         # time without overlap: H2D of the reads, ordering + search on the device copy, D2H of the intervals
@@ -564,15 +678,19 @@ def main():
                                        "output": ev3[2].elapsed_time(ev3[3])}
             # the bound of the end-to-end path: the host->device copy of the reads alone
             sp = line["e2e"]["split_ms"]
-            h2d_rate = Q * world / (sp["input"] * 1e-3)
+            h2d_rate = Q / (sp["input"] * 1e-3)
             line["e2e"]["bound"] = {"kind": "pcie_h2d", "h2d_GBps": h2d / (sp["input"] * 1e-3) / 1e9,
                                     "h2d_only_queries_per_s": h2d_rate,
-                                    "frac": line["e2e"]["value"] / h2d_rate}
+                                    "frac": line["e2e"]["value"] / world / h2d_rate}
             del dwd, outd, permd
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) ----
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, ref, args.cpu_seconds)
+    if rank == 0 and world == 1 and not args.no_cpu and not args.partition:
+        got_h = out.cpu().numpy().view(np.uint32)
+        line["cpu_baseline"] = cpu_baseline(cfg, ref, idx, words_h.numpy().view(np.uint64),
+                                            None if fixed else lens_h.numpy().view(np.uint32), got_h,
+                                            args.cpu_seconds, args.cpu_sample)
+        del got_h
 
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -89,9 +89,12 @@ typedef struct {
 #define SA_INDEX_SUBTABLE 8u
 
 /* sa_match_batch flags. */
-#define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace:
-                              uint32 per query = steps | (text windows fetched << 16); the
-                              workspace must then hold >= 4*Q bytes */
+#define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace (the
+                              workspace must then hold >= 8*Q bytes): uint32 [0, Q) = steps |
+                              (text windows fetched << 16); uint32 [Q, 2Q) = the query's algorithmic
+                              bytes (SURVEY.md Sec. 8(d) "useful bytes": the packed read, the table
+                              entries, 4 B per probed SA entry plus the 2-bit bases from the known
+                              common prefix to the first difference, the 8-byte result) */
 #define SA_MATCH_PRESORT 4u /* order the batch by the reads' first 12 bases (CUB radix sort in the
                                workspace) before the search, so that neighbouring threads walk the
                                same region of the suffix array; results still land at the reads'
@@ -164,9 +167,11 @@ sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uin
                          void *stream);
 
 /* The same match with HOST buffers (page-locked recommended): the queries are
- * streamed host->device in chunks of chunk_Q queries (0 = auto), matched, and
- * the intervals streamed back, with copies and kernels overlapped on internal
- * streams.  Synchronous: out_lohi (host, 2Q uint32) is complete on return. */
+ * streamed host->device in chunks of chunk_Q queries (0 = auto), each chunk ordered
+ * (as sa_match_order, 12 bases) and matched, and the intervals streamed back, with
+ * copies and kernels overlapped on two internal streams.  Synchronous: out_lohi
+ * (host, 2Q uint32) is complete on return, and on an error return no copy into or
+ * out of the caller's buffers is still in flight. */
 sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                               uint32_t stride_words, uint64_t Q, uint32_t *out_lohi, uint64_t chunk_Q);
 

@@ -112,6 +112,17 @@ def _stream_ptr(stream) -> Optional[int]:
     return stream.cuda_stream or None
 
 
+def _empty(shape, dtype, device, stream=None):
+    """torch.empty on `stream` when one is given: the caching allocator then ties the block to the stream
+    the library works on, so a transient freed on return is not handed out again while that stream's
+    kernels still use it."""
+    import torch
+    if stream is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    with torch.cuda.stream(stream):
+        return torch.empty(shape, dtype=dtype, device=device)
+
+
 def _dptr(t) -> Optional[int]:
     return None if t is None else (t.data_ptr() or None)
 
@@ -173,12 +184,12 @@ class Index:
         Q, stride = words.shape
         need = _sz()
         _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(need)), "sa_match_order_workspace_size")
-        ws = torch.empty(max(1, need.value), dtype=torch.uint8, device=words.device)
-        order = torch.empty(Q, dtype=torch.int32, device=words.device)
-        ow = torch.empty_like(words)
-        ol = None if lens is None else torch.empty_like(lens)
+        ws = _empty(max(1, need.value), torch.uint8, words.device, stream)
+        order = _empty(Q, torch.int32, words.device, stream)
+        ow = _empty(tuple(words.shape), words.dtype, words.device, stream)
+        ol = None if lens is None else _empty(tuple(lens.shape), lens.dtype, lens.device, stream)
         nparts = self.part_info()["nparts"]
-        offs = torch.empty(nparts + 1, dtype=torch.int64, device=words.device)
+        offs = _empty(nparts + 1, torch.int64, words.device, stream)
         _check(lib().sa_match_route(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
                                     _dptr(ow), _dptr(ol), _dptr(offs), _dptr(ws), need.value, _stream_ptr(stream)),
                "sa_match_route")
@@ -239,9 +250,9 @@ class Index:
         need = _sz()
         _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(need)), "sa_match_order_workspace_size")
         if workspace is None or workspace.numel() < need.value:
-            workspace = torch.empty(max(1, need.value), dtype=torch.uint8, device=words.device)
+            workspace = _empty(max(1, need.value), torch.uint8, words.device, stream)
         if out is None:
-            out = torch.empty(Q, dtype=torch.int32, device=words.device)
+            out = _empty(Q, torch.int32, words.device, stream)
         _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, int(key_bases),
                                     _dptr(out), _dptr(ordered_words), _dptr(ordered_lens), _dptr(workspace),
                                     need.value, _stream_ptr(stream)), "sa_match_order")
@@ -261,7 +272,8 @@ class Index:
         cooperative: SA_MATCH_COOPERATIVE (reads over 128 bases: 8/16/32 lanes per read).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
-        and, with want_stats, also an int32 tensor [Q] of steps | text windows << 16 (SA_MATCH_STATS).
+        and, with want_stats, also an int32 tensor [2, Q]: row 0 steps | text windows << 16, row 1 the
+        read's algorithmic bytes (SA_MATCH_STATS).
         """
         import torch
         assert words.is_cuda and words.dtype == torch.int64 and words.is_contiguous()
@@ -271,19 +283,19 @@ class Index:
         if lens is not None:
             assert lens.is_cuda and lens.dtype == torch.int32 and lens.numel() == Q and lens.is_contiguous()
         if out is None:
-            out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
+            out = _empty((Q, 2), torch.int32, words.device, stream)
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
         flags = (SA_MATCH_STATS if want_stats else 0) | (SA_MATCH_PRESORT if presort else 0) | \
                 (SA_MATCH_ROWS_ORDERED if rows_ordered else 0) | (SA_MATCH_COOPERATIVE if cooperative else 0)
         need = self.workspace_size(Q, stride, flags) \
             if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
         if need and (workspace is None or workspace.numel() < need):
-            workspace = torch.empty(need, dtype=torch.uint8, device=words.device)
+            workspace = _empty(need, torch.uint8, words.device, stream)
         _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
                                     _dptr(out), _dptr(workspace) if need else None, need, flags, _stream_ptr(stream)),
                "sa_match_batch")
-        if want_stats:
-            return out, workspace[: 4 * Q].view(torch.int32)
+        if want_stats:  # [2, Q]: row 0 steps | text windows << 16, row 1 algorithmic bytes (include/sa.h)
+            return out, workspace[: 8 * Q].view(torch.int32).view(2, Q)
         return out
 
     def match_host(self, words: np.ndarray, lens: Optional[np.ndarray] = None, fixed_len: Optional[int] = None,
@@ -306,10 +318,10 @@ class Index:
         """sa_locate_offsets: exclusive prefix sum of the counts (CUDA int64 [Q+1]); offsets[Q] = total."""
         import torch
         Q = lohi.shape[0]
-        offsets = torch.empty(Q + 1, dtype=torch.int64, device=lohi.device)
+        offsets = _empty(Q + 1, torch.int64, lohi.device, stream)
         ws = _sz()
         _check(lib().sa_locate_workspace_size(Q, ctypes.byref(ws)), "sa_locate_workspace_size")
-        wsb = torch.empty(max(1, ws.value), dtype=torch.uint8, device=lohi.device)
+        wsb = _empty(max(1, ws.value), torch.uint8, lohi.device, stream)
         _check(lib().sa_locate_offsets(self._h, _dptr(lohi), Q, _dptr(offsets), _dptr(wsb), ws.value,
                                        _stream_ptr(stream)), "sa_locate_offsets")
         return offsets
@@ -320,7 +332,9 @@ class Index:
         import torch
         Q = lohi.shape[0] if n_reads is None else int(n_reads)
         if out is None:
-            out = torch.empty(int(offsets[Q].item()), dtype=torch.int32, device=lohi.device)
+            if stream is not None:  # offsets were written on `stream`: wait for it before reading the total
+                stream.synchronize()
+            out = _empty(int(offsets[Q].item()), torch.int32, lohi.device, stream)
         positions = out
         _check(lib().sa_locate(self._h, _dptr(lohi), _dptr(offsets), Q, _dptr(positions), _stream_ptr(stream)),
                "sa_locate")
@@ -359,7 +373,7 @@ class Tree:
         import torch
         Q, stride = words.shape
         if out is None:
-            out = torch.empty((Q, 2), dtype=torch.int32, device=words.device)
+            out = _empty((Q, 2), torch.int32, words.device, stream)
         _check(lib().sa_tree_match(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
                                    _dptr(out), _stream_ptr(stream)), "sa_tree_match")
         return out

@@ -35,6 +35,8 @@ static void free_index(sa_index *idx) {
         cudaFree(idx->pipe_words[b]);
         cudaFree(idx->pipe_lens[b]);
         cudaFree(idx->pipe_out[b]);
+        cudaFree(idx->pipe_order[b]);
+        cudaFree(idx->pipe_ws[b]);
         if (idx->pipe_stream[b]) cudaStreamDestroy(idx->pipe_stream[b]);
     }
     (void)cudaGetLastError();

@@ -159,13 +159,17 @@ __device__ __forceinline__ uint64_t big_hash(uint32_t x, uint32_t bits) {
     return (uint64_t)((x * 0x9E3779B1u) >> (32 - bits));
 }
 
-__global__ void k_big_hash_insert(const uint32_t *__restrict__ big, uint64_t cnt, uint32_t bits, uint2 *__restrict__ H) {
+// Slots are 64-bit {x << 32 | sub-table id}, published by ONE atomicCAS; the empty slot is ~0, which no
+// entry can equal (ids are < 2^26), so every k-mer -- including the all-T bucket 0xFFFFFFFF at k = 16 --
+// is a valid key.
+__global__ void k_big_hash_insert(const uint32_t *__restrict__ big, uint64_t cnt, uint32_t bits,
+                                  unsigned long long *__restrict__ H) {
     GRID_STRIDE(id, cnt) {
         const uint32_t x = big[id];
         const uint64_t mask = (1ull << bits) - 1;
+        const unsigned long long e = ((unsigned long long)x << 32) | (uint32_t)id;
         for (uint64_t h = big_hash(x, bits);; h = (h + 1) & mask) {
-            const unsigned prev = atomicCAS(&H[h].x, 0xFFFFFFFFu, x);
-            if (prev == 0xFFFFFFFFu) { H[h].y = (uint32_t)id; break; }
+            if (atomicCAS(&H[h], kBigEmpty, e) == kBigEmpty) break;
         }
     }
 }
@@ -454,8 +458,8 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
             uint32_t bits = 1;
             while ((1ull << bits) < 2ull * (uint64_t)total) ++bits;
             SA_CUDA_TRY(cudaMalloc(&idx->big_sub, (uint64_t)total * 257 * sizeof(uint32_t)));
-            SA_CUDA_TRY(cudaMalloc(&idx->big_hash, (1ull << bits) * sizeof(uint2)));
-            SA_CUDA_TRY(cudaMemsetAsync(idx->big_hash, 0xFF, (1ull << bits) * sizeof(uint2), st));
+            SA_CUDA_TRY(cudaMalloc(&idx->big_hash, (1ull << bits) * sizeof(unsigned long long)));
+            SA_CUDA_TRY(cudaMemsetAsync(idx->big_hash, 0xFF, (1ull << bits) * sizeof(unsigned long long), st));
             k_big_hash_insert<<<grid_for((uint64_t)total), kThreads, 0, st>>>(big.p, (uint64_t)total, bits, idx->big_hash);
             SA_CUDA_TRY(cudaGetLastError());
             k_big_subtables<<<(unsigned)total, 128, 0, st>>>(idx->text, n, idx->sa, idx->k, idx->table, big.p,

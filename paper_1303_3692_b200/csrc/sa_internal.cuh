@@ -72,6 +72,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------------------------
 // the index (immutable after create)
 constexpr uint32_t kBigBucket = 32;  // SA_INDEX_SUBTABLE threshold (suffixes per k-mer bucket)
+constexpr unsigned long long kBigEmpty = ~0ull;  // empty sub-table hash slot (no {x, id} entry equals it)
 constexpr uint64_t kGuardWords = 6;  // zero words past the text: windows up to base n + 159 are readable
 
 // SA values of the layout: base pointer + stride in uint32 units
@@ -96,7 +97,7 @@ struct sa_index {
     bool subtables = false;
     uint64_t big_count = 0;      // large buckets
     uint32_t big_bits = 0;       // log2 of the hash table size
-    uint2 *big_hash = nullptr;   // dev: open addressing {bucket x, sub-table id}, empty = {~0, ~0}
+    unsigned long long *big_hash = nullptr;  // dev: open addressing, x << 32 | sub-table id, empty = kBigEmpty
     uint32_t *big_sub = nullptr; // dev: big_count x 257 global SA ranks
     // partitioned index (sa_index_create_part): this index holds SA ranks [rank_base, rank_end) and
     // table entries [x_base, x_end] only, i.e. the reads whose first route_bases bases lie in
@@ -110,6 +111,9 @@ struct sa_index {
     uint64_t *pipe_words[2] = {nullptr, nullptr};
     uint32_t *pipe_lens[2] = {nullptr, nullptr};
     uint32_t *pipe_out[2] = {nullptr, nullptr};
+    uint32_t *pipe_order[2] = {nullptr, nullptr};  // per-chunk read ordering (a5)
+    void *pipe_ws[2] = {nullptr, nullptr};         // its sort workspace
+    size_t pipe_ws_bytes = 0;
     uint64_t pipe_chunk = 0;
     uint64_t pipe_words_cap = 0;
 };
@@ -164,6 +168,14 @@ __device__ __forceinline__ void ld_v2u64(const void *p, uint64_t &a, uint64_t &b
 // 256-bit load (sm_100): LDG.E.ENL2.256
 __device__ __forceinline__ void ld_v4u64(const void *p, uint64_t &a, uint64_t &b, uint64_t &c, uint64_t &d) {
     asm(SA_LD_OP ".v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
+// a load the compiler may not merge with an earlier load of the same address (re-reads a value instead
+// of keeping it live in a register)
+__device__ __forceinline__ uint32_t reload_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
 }
 
 // 32 bases of the packed text starting at base b (b < n + 32); bases past n read as 0 ('a').

@@ -79,13 +79,14 @@ __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_
 }
 
 // row t of the ordered copy = read order[t] (coalesced writes; the reads are gathered once here)
+// (vec: one 256-bit copy per row; the caller sets it only for stride 4 with both buffers 32-byte aligned)
 __global__ void k_gather_rows(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens, uint32_t stride,
-                              uint64_t Q, const uint32_t *__restrict__ order, uint64_t *__restrict__ out_words,
+                              bool vec, uint64_t Q, const uint32_t *__restrict__ order, uint64_t *__restrict__ out_words,
                               uint32_t *__restrict__ out_lens) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t q = __ldg(order + t);
         if (out_words) {
-            if (stride == 4) {
+            if (vec) {
                 reinterpret_cast<ulonglong4 *>(out_words)[t] = reinterpret_cast<const ulonglong4 *>(words)[q];
             } else {
                 for (uint32_t j = 0; j < stride; ++j) out_words[t * stride + j] = __ldg(words + q * stride + j);
@@ -105,7 +106,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // sa_match_batch (stats first, then, with SA_MATCH_PRESORT, the same sort scratch + the permutation)
 sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, PresortLayout &L) {
     size_t off = 0;
-    if (stats) { L.stats = off; off = align256(off + Q * 4); }
+    if (stats) { L.stats = off; off = align256(off + Q * 8); }
     if (presort) {
         if (Q >= (1ull << 32)) { sa_set_error("read ordering needs Q < 2^32"); return SA_EINVAL; }
         L.keys_in = off; off = align256(off + Q * 4);
@@ -307,8 +308,8 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
                          (reinterpret_cast<uintptr_t>(ordered_words) & 31) == 0;
         uint64_t blocks = (Q + 255) / 256;
         if (blocks > 148ull * 16) blocks = 148ull * 16;
-        k_gather_rows<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(q_words, q_len, vec ? 4u : stride_words, Q,
-                                                                          order, ordered_words, ordered_len);
+        k_gather_rows<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(q_words, q_len, stride_words, vec, Q, order,
+                                                                          ordered_words, ordered_len);
         SA_CUDA_TRY(cudaGetLastError());
     }
     return SA_OK;
@@ -406,6 +407,16 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
                         (flags & SA_MATCH_COOPERATIVE) != 0);
 }
 
+// Synchronises the host pipeline's streams when sa_match_batch_host returns, on success and on every
+// error path, so no copy into or out of the caller's host buffers outlives the call.
+struct PipeSyncGuard {
+    sa_index *idx;
+    ~PipeSyncGuard() {
+        for (int b = 0; b < 2; ++b)
+            if (idx->pipe_stream[b]) cudaStreamSynchronize(idx->pipe_stream[b]);
+    }
+};
+
 extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
                                          uint32_t fixed_len, uint32_t stride, uint64_t Q, uint32_t *out_lohi,
                                          uint64_t chunk_Q) {
@@ -420,27 +431,40 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
     // words of `cq` reads starting at read q0 (q0 a multiple of chunk_Q, hence of 32 for dense)
     auto words_of = [&](uint64_t cq) { return stride ? cq * stride : (cq * (uint64_t)fixed_len + 31) / 32; };
     const uint64_t need_words = words_of(chunk_Q);
-    if (idx->pipe_chunk < chunk_Q || idx->pipe_words_cap < need_words) {
+    PresortLayout OL;
+    SA_TRY(presort_layout(chunk_Q, false, true, true, OL));
+    for (int b = 0; b < 2; ++b)
+        if (!idx->pipe_stream[b]) SA_CUDA_TRY(cudaStreamCreateWithFlags(&idx->pipe_stream[b], cudaStreamNonBlocking));
+    PipeSyncGuard guard{idx};
+    if (idx->pipe_chunk < chunk_Q || idx->pipe_words_cap < need_words || idx->pipe_ws_bytes < OL.total) {
         for (int b = 0; b < 2; ++b) {
             cudaFree(idx->pipe_words[b]);
             cudaFree(idx->pipe_lens[b]);
             cudaFree(idx->pipe_out[b]);
+            cudaFree(idx->pipe_order[b]);
+            cudaFree(idx->pipe_ws[b]);
             idx->pipe_words[b] = nullptr;
             idx->pipe_lens[b] = nullptr;
             idx->pipe_out[b] = nullptr;
+            idx->pipe_order[b] = nullptr;
+            idx->pipe_ws[b] = nullptr;
         }
         idx->pipe_chunk = 0;
         idx->pipe_words_cap = 0;
+        idx->pipe_ws_bytes = 0;
         for (int b = 0; b < 2; ++b) {
-            if (!idx->pipe_stream[b]) SA_CUDA_TRY(cudaStreamCreateWithFlags(&idx->pipe_stream[b], cudaStreamNonBlocking));
             SA_CUDA_TRY(cudaMalloc(&idx->pipe_words[b], need_words * sizeof(uint64_t)));
             SA_CUDA_TRY(cudaMalloc(&idx->pipe_lens[b], chunk_Q * sizeof(uint32_t)));
             SA_CUDA_TRY(cudaMalloc(&idx->pipe_out[b], chunk_Q * 2 * sizeof(uint32_t)));
+            SA_CUDA_TRY(cudaMalloc(&idx->pipe_order[b], chunk_Q * sizeof(uint32_t)));
+            SA_CUDA_TRY(cudaMalloc(&idx->pipe_ws[b], OL.total));
         }
         idx->pipe_chunk = chunk_Q;
         idx->pipe_words_cap = need_words;
+        idx->pipe_ws_bytes = OL.total;
     }
-    // chunk c uses buffer set c%2 on stream c%2: H2D -> match -> D2H; the two streams overlap.
+    // chunk c uses buffer set c%2 on stream c%2: H2D -> order (a5) -> match (a6-a9) -> D2H; the two
+    // streams overlap, so one chunk's copies run under the other's kernels.
     uint64_t c = 0;
     for (uint64_t q0 = 0; q0 < Q; q0 += chunk_Q, ++c) {
         const int b = (int)(c & 1);
@@ -454,8 +478,12 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, nullptr,
-                            false, st));
+        PresortLayout L;
+        SA_TRY(presort_layout(cq, false, true, true, L));
+        SA_TRY(order_reads(idx->pipe_words[b], dl, fixed_len, stride, cq, kDefaultKeyBases,
+                           static_cast<uint8_t *>(idx->pipe_ws[b]), L, idx->pipe_order[b], st));
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr,
+                            idx->pipe_order[b], false, st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }
@@ -494,7 +522,7 @@ extern "C" sa_status sa_match_route(const sa_index *idx, const uint64_t *q_words
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     const bool vec = stride_words == 4 && (reinterpret_cast<uintptr_t>(q_words) & 31) == 0 &&
                      (reinterpret_cast<uintptr_t>(ordered_words) & 31) == 0;
-    k_gather_rows<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, vec ? 4u : stride_words, Q, order, ordered_words,
+    k_gather_rows<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, stride_words, vec, Q, order, ordered_words,
                                                    ordered_len);
     SA_CUDA_TRY(cudaGetLastError());
     DevBuf<uint32_t> bounds;

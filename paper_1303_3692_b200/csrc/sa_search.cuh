@@ -35,13 +35,13 @@ struct MatchArgs {
     uint32_t stride;
     uint64_t Q;
     uint32_t *__restrict__ out;
-    uint32_t *__restrict__ stats;       // SA_MATCH_STATS
+    uint32_t *__restrict__ stats;       // SA_MATCH_STATS: [Q] steps | text windows << 16, [Q] useful bytes
     const uint32_t *__restrict__ order; // thread slot t takes read order[t] (or t)
     bool vec_rows;                      // read rows can be loaded with one vector load (aligned, stride == QW)
     uint64_t dense_words;               // stride == 0: dense layout, words = one 2-bit stream of this many words
     bool rows_ordered;                  // SA_MATCH_ROWS_ORDERED: row t is read order[t]
     uint32_t min_len;                   // partitioned index: reads shorter than k get (~0, ~0)
-    const uint2 *__restrict__ big_hash; // SA_INDEX_SUBTABLE: {bucket, sub-table id}, empty = {~0, ~0}
+    const unsigned long long *__restrict__ big_hash; // SA_INDEX_SUBTABLE: x << 32 | sub-table id, empty = ~0
     const uint32_t *__restrict__ big_sub;
     uint32_t big_bits;
 };
@@ -541,16 +541,26 @@ __device__ __forceinline__ void probe(const MatchArgs &a, const RD &P, uint32_t 
 }
 
 // Binary search over (Lp1-1, R): LB rule (lower: R moves when P <= t) or RB rule (R moves when P < t).
+// SA_MATCH_STATS: the algorithmic bytes of one probe (SURVEY.md Sec. 8(d) "useful bytes"): the 4-byte SA
+// entry plus the bases that decide the compare, from the known common prefix `skip` up to and including
+// the first difference (all m - skip bases when P is a prefix of the suffix), 2 bits each.
+__device__ __forceinline__ uint32_t probe_bytes(uint32_t m, uint32_t skip, uint32_t lcp) {
+    const uint32_t end = lcp + 1 < m ? lcp + 1 : m;
+    return 4u + (end > skip ? (end - skip + 3) >> 2 : 0u);
+}
+
 template <int L, class RD>
 __device__ __forceinline__ uint32_t bound(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1,
                                           uint32_t R, uint32_t lcpL, uint32_t lcpR, bool lower, bool in_bracket,
-                                          uint32_t &steps, uint32_t &texts) {
+                                          uint32_t &steps, uint32_t &texts, uint32_t &ubytes) {
     while (R > Lp1) {
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
-        probe<L>(a, P, m, p, min(lcpL, lcpR), in_bracket, sign, lcp, texts);
+        const uint32_t skip = min(lcpL, lcpR);
+        probe<L>(a, P, m, p, skip, in_bracket, sign, lcp, texts);
         ++steps;
+        ubytes += probe_bytes(m, skip, lcp);
         if (sign < 0 || (lower && sign == 0)) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
     }
     return R;
@@ -559,7 +569,7 @@ __device__ __forceinline__ uint32_t bound(const MatchArgs &a, const RD &P, uint3
 // One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.
 template <int L, class RD>
 __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uint32_t m, uint32_t &lo,
-                                            uint32_t &hi, uint32_t &steps, uint32_t &texts) {
+                                            uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes) {
     const uint32_t k = a.k;
     if (m == 0) {  // the empty read is a prefix of every suffix (reading A12)
         lo = 0;
@@ -572,28 +582,30 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
         const uint64_t x = P.first() >> (64 - 2 * m);
         const uint32_t Ta = ld_u32(a.table + (x << (2 * (k - m))));
         const uint32_t Tb = ld_u32(a.table + ((x + 1) << (2 * (k - m))));
-        lo = bound<L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts);
-        hi = bound<L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts);
+        ubytes += 8;  // the two table entries
+        lo = bound<L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts, ubytes);
+        hi = bound<L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts, ubytes);
         return;
     }
     // all suffixes before T[x] are < P, all from T[x+1] on are > P
     const uint64_t x = P.first() >> (64 - 2 * k);
     uint32_t Lp1, R;
     table_pair(a.table, x, Lp1, R);
+    ubytes += 8;  // T[x], T[x+1]
     if (a.big_sub && R - Lp1 > kBigBucket && m >= k + 4) {
         // a large bucket (repeats): its (k+4)-base sub-table narrows the bracket by the next 4 bases
         const uint64_t mask = (1ull << a.big_bits) - 1;
         uint64_t h = (uint64_t)(((uint32_t)x * 0x9E3779B1u) >> (32 - a.big_bits));
         for (uint64_t tries = 0; tries <= mask; ++tries, h = (h + 1) & mask) {
-            const uint2 e = ld_v2u32(a.big_hash + h);
-            if (e.x == (uint32_t)x) {
-                const uint32_t *T2 = a.big_sub + (uint64_t)e.y * 257;
+            const uint64_t e = ld_u64(reinterpret_cast<const uint64_t *>(a.big_hash) + h);
+            if (e == ~0ull) break;  // empty slot: x has no sub-table (tested before the key)
+            if ((uint32_t)(e >> 32) == (uint32_t)x) {
+                const uint32_t *T2 = a.big_sub + (uint64_t)(uint32_t)e * 257;
                 const uint32_t y = (uint32_t)(after_k0(P, k) >> 56);  // bases k .. k+3
                 Lp1 = ld_u32(T2 + y);
                 R = ld_u32(T2 + y + 1);
                 break;
             }
-            if (e.x == 0xFFFFFFFFu) break;
         }
     }
     uint32_t lcpL = 0, lcpR = 0;
@@ -603,8 +615,10 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
-        probe<L>(a, P, m, p, min(lcpL, lcpR), true, sign, lcp, texts);
+        const uint32_t skip = min(lcpL, lcpR);
+        probe<L>(a, P, m, p, skip, true, sign, lcp, texts);
         ++steps;
+        ubytes += probe_bytes(m, skip, lcp);
         if (sign == 0) {  // lo lies in (L, p], hi in (p, R]: the RB search starts from here
             split = true;
             hLp1 = p + 1; hR = R; hlcpL = lcp; hlcpR = lcpR;
@@ -619,8 +633,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
     }
     // finish the LB search in (L, p], then the RB search in (p, R at the split].  (Interleaving the
     // two chains, both probes issued before either compare, measured 3% slower at C4: profiles/r01n.)
-    lo = bound<L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts);
-    hi = bound<L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts);
+    lo = bound<L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts, ubytes);
+    hi = bound<L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts, ubytes);
 }
 
 __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
@@ -644,34 +658,44 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 #ifndef SA_MATCH_THREADS
 #define SA_MATCH_THREADS 256  // block size of k_match (A/B builds: variants/)
 #endif
-#ifdef SA_MATCH_MINB  // minimum resident blocks per SM requested from ptxas (a register cap)
-#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS, SA_MATCH_MINB)
-#else
-#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS)
+// minimum resident blocks per SM requested from ptxas (a register cap): 5 x 256 threads = 62.5%
+// occupancy = at most 48 registers, the plateau measured in r01-3 (profiles/r01-3/e_*: 40 registers
+// spill and run slower, 64 registers (50%) run 9% slower)
+#ifndef SA_MATCH_MINB
+#define SA_MATCH_MINB (1280 / SA_MATCH_THREADS)
 #endif
+// (the long-read instantiation, QW = 0, keeps ptxas's own choice: capped it spills)
+#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS, QW > 0 ? SA_MATCH_MINB : 1)
 template <int QW, int L, bool STATS>
 __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.Q) return;
-    const uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;  // the read; its result goes to out[q]
-    const uint64_t row = a.rows_ordered ? t : q;                      // where its bases are
+    uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;  // the read; its result goes to out[q]
+    const uint64_t row = a.rows_ordered ? t : q;               // where its bases are
     const uint32_t m = read_len(a, row);
     QueryWords<QW> P;
     load_read<QW>(a, row, m, P);
-    uint32_t lo, hi, steps = 0, texts = 0;
+    // ubytes (SA_MATCH_STATS): the read (2 bits/base) + the 8-byte result + what the search adds
+    uint32_t lo, hi, steps = 0, texts = 0, ubytes = ((m + 3) >> 2) + 8;
     if (m < a.min_len) {  // a partition cannot answer a read shorter than k (its window may leave the slice)
         lo = hi = 0xFFFFFFFFu;
     } else {
-        search_read<L>(a, P, m, lo, hi, steps, texts);
+        search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
     }
-    // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here
+    // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here.
+    // The read index is loaded again here (an L1 hit) rather than kept live across the search: at the
+    // 48 registers of the 62.5%-occupancy build ptxas otherwise spills it to local memory.
+    if (a.order) q = reload_u32(a.order + t);
 #ifdef SA_OUT_PAD  // experiment: one full 32-byte sector per read (no ECC read-modify-write of a partial sector)
     reinterpret_cast<uint4 *>(a.out)[2 * q] = make_uint4(lo, hi, 0u, 0u);
     reinterpret_cast<uint4 *>(a.out)[2 * q + 1] = make_uint4(0u, 0u, 0u, 0u);
 #else
     reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
 #endif
-    if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+    if (STATS) {
+        a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+        a.stats[a.Q + q] = ubytes;
+    }
 }
 
 // Long reads (m > 128): G lanes per read slot (GroupRead), the same search as k_match.
@@ -689,15 +713,18 @@ __global__ void __launch_bounds__(256) k_match_group(const MatchArgs a) {
     } else {
         P.init(a.words + row * a.stride, 0u, ~0ull, (m + 31) >> 5);
     }
-    uint32_t lo, hi, steps = 0, texts = 0;
+    uint32_t lo, hi, steps = 0, texts = 0, ubytes = ((m + 3) >> 2) + 8;
     if (m < a.min_len) {
         lo = hi = 0xFFFFFFFFu;
     } else {
-        search_read<L>(a, P, m, lo, hi, steps, texts);
+        search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
     }
     if (P.lane == 0) {
         reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
-        if (STATS) a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+        if (STATS) {
+            a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+            a.stats[a.Q + q] = ubytes;
+        }
     }
 }
 

@@ -4,7 +4,8 @@ report needs: an all_reduce(MAX) of elapsed device time and an all_gather of per
 Everything here is backend-agnostic (NCCL on the B200 box, gloo in the CPU tests)."""
 from __future__ import annotations
 
-from typing import List, Tuple
+import os
+from typing import List, Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -12,11 +13,59 @@ import torch.distributed as dist
 GOLDEN = 0x9E3779B1
 
 
-def shard(rank: int, world: int, reads_per_rank: int) -> Tuple[int, int]:
-    """Weak scaling: rank r matches reads [r*Q, (r+1)*Q) of the seeded read stream."""
+def shard(rank: int, world: int, reads: int, weak: bool = False) -> Tuple[int, int]:
+    """(q_begin, q_count) of rank's reads in the seeded read stream.
+
+    Strong scaling (default: "Q is split into g contiguous equal slices"): the job's
+    `reads` are cut into `world` contiguous slices whose sizes differ by at most one.
+    Weak scaling (opt-in): every rank matches its own `reads` reads, [rank*reads, (rank+1)*reads)."""
     if not (0 <= rank < world):
         raise ValueError("rank out of range")
-    return rank * reads_per_rank, reads_per_rank
+    if weak:
+        return rank * reads, reads
+    b = rank * reads // world
+    return b, (rank + 1) * reads // world - b
+
+
+def parse_cpulist(s: str) -> List[int]:
+    """'0-3,8,10-11' -> [0, 1, 2, 3, 8, 10, 11] (the sysfs cpulist format)."""
+    out: List[int] = []
+    for part in s.strip().split(","):
+        if not part:
+            continue
+        if "-" in part:
+            a, b = part.split("-")
+            out.extend(range(int(a), int(b) + 1))
+        else:
+            out.append(int(part))
+    return out
+
+
+def gpu_local_cpus(device_index: int) -> Optional[List[int]]:
+    """The host CPUs on the GPU's own NUMA node (sysfs local_cpulist of its PCI function), or None."""
+    try:
+        p = torch.cuda.get_device_properties(device_index)
+        bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
+            cpus = parse_cpulist(f.read())
+        return cpus or None
+    except Exception:
+        return None
+
+
+def bind_numa_local(device_index: int) -> dict:
+    """Pin this rank's process to the CPUs local to its GPU, so the pinned host buffers it allocates and
+    first-touches afterwards (reads, results, the e2e staging) are placed on the GPU's NUMA node.
+    Returns what was done, for the bench line."""
+    cpus = gpu_local_cpus(device_index)
+    if not cpus:
+        return {"bound": False, "reason": "no local_cpulist for the GPU"}
+    allowed = os.sched_getaffinity(0)
+    use = sorted(set(cpus) & allowed)
+    if not use:
+        return {"bound": False, "reason": "GPU-local CPUs outside this process's affinity"}
+    os.sched_setaffinity(0, use)
+    return {"bound": True, "cpus": len(use), "first": use[0], "last": use[-1]}
 
 
 def summarize(lohi: torch.Tensor) -> torch.Tensor:
@@ -36,6 +85,17 @@ def max_over_ranks(value: float, device) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def all_reduce_sum(value: int, device) -> int:
+    """Sum of a per-rank integer (reads matched) over the default group; identity when not distributed."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return int(value)
+    if dist.get_backend() != "nccl":
+        device = "cpu"
+    t = torch.tensor([value], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
 
 
 def gather_summaries(summary: torch.Tensor) -> List[List[int]]:

@@ -34,7 +34,7 @@ def _intervals(q_begin, q_count):
 def _worker(rank, world, port, outq):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    q0, qn = shard.shard(rank, world, Q_RANK)
+    q0, qn = shard.shard(rank, world, world * Q_RANK + 1)  # strong: contiguous slices of one job
     summ = shard.summarize(_intervals(q0, qn))
     gathered = shard.gather_summaries(summ)
     elapsed = shard.max_over_ranks(10.0 * (rank + 1), "cpu")
@@ -59,12 +59,26 @@ def test_two_rank_gloo_matches_single_process():
     assert res[0][1] == res[1][1]
     assert res[0][2] == res[1][2] == 20.0
     # shards are the contiguous slices of one read stream: combined == single-process summary
-    single = shard.summarize(_intervals(0, world * Q_RANK)).tolist()
+    single = shard.summarize(_intervals(0, world * Q_RANK + 1)).tolist()
     assert shard.combine(res[0][1]) == single
 
 
 def test_shard_ranges():
-    assert shard.shard(0, 4, 100) == (0, 100)
-    assert shard.shard(3, 4, 100) == (300, 100)
+    # strong scaling (default): contiguous slices of the job's reads that tile [0, Q)
+    assert shard.shard(0, 4, 100) == (0, 25)
+    assert shard.shard(3, 4, 100) == (75, 25)
+    for Q in (0, 1, 7, 100_000_001):
+        for world in (1, 2, 3, 8):
+            sl = [shard.shard(r, world, Q) for r in range(world)]
+            assert sl[0][0] == 0 and sum(c for _, c in sl) == Q
+            assert all(a + c == b for (a, c), (b, _) in zip(sl, sl[1:]))
+            assert max(c for _, c in sl) - min(c for _, c in sl) <= 1
+    # weak scaling (opt-in): every rank its own Q reads
+    assert shard.shard(3, 4, 100, weak=True) == (300, 100)
     with pytest.raises(ValueError):
         shard.shard(4, 4, 100)
+
+
+def test_cpulist_parse():
+    assert shard.parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert shard.parse_cpulist("5") == [5]

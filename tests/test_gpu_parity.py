@@ -135,6 +135,19 @@ def test_subtables_for_large_buckets(k, layout):
         check_full(text, hazard_queries(text, k, rng, extra=400), k=k, layout=layout, subtables=True)
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_subtables_k16_all_t_bucket(layout):
+    # k = 16: the all-T bucket's k-mer is 0xFFFFFFFF.  A poly-T run of 300 bases puts 285 suffixes in it
+    # (> 32: it gets a sub-table), next to poly-A (bucket 0) and other large buckets.
+    rng = random.Random(16)
+    rnd = lambda n: "".join(rng.choice("ACGT") for _ in range(n))
+    text = rnd(5000) + "T" * 300 + rnd(3000) + "A" * 200 + rnd(2000) + "TTTTTTTTTTTTTTTTG" * 40 + rnd(1000) + "T" * 60
+    qs = hazard_queries(text, 16, rng, extra=300)
+    qs += ["T" * m for m in range(14, 320, 3)] + ["T" * m + "G" for m in range(15, 70, 4)]
+    qs += ["A" * m for m in range(14, 220, 5)] + ["TTTTTTTTTTTTTTTTG" * r for r in (1, 2, 5, 41)]
+    check_full(text, qs, k=16, layout=layout, subtables=True)
+
+
 def test_subtables_repeat_rich():
     ref = synth.reference(synth.REF_REPEAT, 3_000_000, 35)
     words, lens = synth.reads(ref, 200_000, 16, 160, 0.1, 0.01, 36)
@@ -243,9 +256,15 @@ def test_stats_iteration_bound():
     got, st = gpu_match(idx, words, lens, want_stats=True)
     S = oracle.encode(ref)
     assert np.array_equal(got, oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32))
-    steps = st & 0xFFFF
+    steps = st[0] & 0xFFFF
     import math
     assert steps.max() <= 2 * math.ceil(math.log2(len(ref) + 2))
+    # algorithmic bytes: at least the packed read + table pair + result, at most 4 + ceil(m/4) + 1 per step
+    ub = st[1].astype(np.int64)
+    m = lens.astype(np.int64)
+    floor = (m + 3) // 4 + 8
+    assert np.all(ub >= floor)
+    assert np.all(ub <= floor + 8 + steps * (4 + (m + 3) // 4 + 1))
 
 
 @pytest.mark.parametrize("key_bases", [0, 8, 16])

@@ -37,6 +37,7 @@ del words
 perm = idx.order(w, None, fixed_len=100)
 ws = w[perm.long()].contiguous()          # rows in order
 _, st = idx.match(ws, None, fixed_len=100, want_stats=True)
+st = st[0]
 steps = (st.view(torch.int32).to(torch.int64) & 0xFFFF)
 res = {"Q": Q, "all_ms": timed(idx, ws), "classes": []}
 for lo, hi in [(0, 0), (1, 1), (2, 2), (3, 4), (5, 8), (9, 16), (17, 64)]:

@@ -13,6 +13,7 @@ words, lens = cfg.reads(ref, q_count=20_000_000)
 w = torch.from_numpy(words.view(np.int64)).cuda()
 perm = idx.order(w, None, fixed_len=100)
 out, st = idx.match(w, None, fixed_len=100, order=perm, want_stats=True)
+st = st[0]
 steps = (st.cpu().numpy().view(np.uint32) & 0xFFFF).astype(np.int64)
 lohi = out.cpu().numpy().view(np.uint32).astype(np.int64)
 cnt = lohi[:, 1] - lohi[:, 0]
