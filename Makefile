@@ -35,7 +35,8 @@ VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ld
             variants/libsa_l2_64na.so variants/libsa_t128.so variants/libsa_t64.so variants/libsa_t128_m12.so \
             variants/libsa_t64_m32.so variants/libsa_t256_m6.so variants/libsa_t64_m24.so variants/libsa_t128_m10.so \
             variants/libsa_t64_m20.so variants/libsa_t256_m1.so variants/libsa_outpad.so variants/libsa_t256_m5.so \
-            variants/libsa_head1.so variants/libsa_head2.so variants/libsa_head3.so variants/libsa_head1_m5.so
+            variants/libsa_head1.so variants/libsa_head2.so variants/libsa_head3.so variants/libsa_head1_m5.so \
+            variants/libsa_bulkpf.so
 variants/libsa_ldcg.so: DEFS := -DSA_LD_MODE=1
 variants/libsa_ldnoalloc.so: DEFS := -DSA_LD_MODE=2
 variants/libsa_ldca.so: DEFS := -DSA_LD_MODE=3
@@ -56,6 +57,7 @@ variants/libsa_head1.so: DEFS := -DSA_QW0_HEAD=1
 variants/libsa_head2.so: DEFS := -DSA_QW0_HEAD=2
 variants/libsa_head3.so: DEFS := -DSA_QW0_HEAD=3
 variants/libsa_head1_m5.so: DEFS := -DSA_QW0_HEAD=1 -DSA_MATCH_MINB=5
+variants/libsa_bulkpf.so: DEFS := -DSA_BULK_PREFETCH
 variants: $(VARIANTS)
 variants/%.so: $(CU_SRCS) $(CU_HDRS)
 	mkdir -p variants && $(NVCC) $(NVFLAGS) $(DEFS) -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_$(notdir $@).log || (cat build/ptxas_$(notdir $@).log; false)

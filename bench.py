@@ -78,6 +78,9 @@ def parse():
                     help="the ordering step also gathers the read rows into order (SA_MATCH_ROWS_ORDERED)")
     ap.add_argument("--cooperative", action="store_true",
                     help="SA_MATCH_COOPERATIVE: reads over 128 bases searched by 8/16/32-lane groups")
+    ap.add_argument("--smem-tree", type=int, default=0,
+                    help="SA_MATCH_SMEM_TREE: levels (1..12) of the per-CTA shared-memory top tree staged by TMA "
+                         "(SURVEY.md 8(a) a3(ii)); 0 = off")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -312,7 +315,8 @@ def cpu_baseline(cfg, ref, idx, words, lens, got, seconds, max_sample):
     d1 = time.perf_counter() - t
     sa_ = min(max_sample, Q)
     t = time.perf_counter()
-    ra = oracle.search_batch(S, sa_host, words[:sa_], None if lw is None else lw[:sa_], fixed_len=cfg.m_max, nthreads=0)
+    ra = oracle.search_batch(S, sa_host, words[:sa_], None if lw is None else lw[:sa_], fixed_len=cfg.m_max,
+                             nthreads=cores)  # (explicit: the 1-thread call left OpenMP at 1 thread)
     da = time.perf_counter() - t
     agree = bool(np.array_equal(ra.astype(np.uint32), got[:sa_]) and np.array_equal(r1.astype(np.uint32), got[:s1]))
     v1, va = s1 / d1, sa_ / da
@@ -443,7 +447,7 @@ def main():
                       cooperative=args.cooperative)
         else:
             idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm,
-                      cooperative=args.cooperative)
+                      cooperative=args.cooperative, smem_tree=args.smem_tree, tree_key_bases=args.order_bases)
         if i is not None:
             ev[i][1].record(stream)
 
@@ -493,7 +497,7 @@ def main():
             "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
                                           if presort else 0),
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
-            "shards": summary_all, "layout": args.layout, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
+            "shards": summary_all, "layout": args.layout, "smem_tree_levels": args.smem_tree, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
             "index_bytes": idx.device_bytes,
             "index_build": {"seconds": build_s, "sa_algorithm": args.build,
                             "note": "untimed: upload + pack + suffix array + k-mer table + records"}}

@@ -107,6 +107,16 @@ typedef struct {
                                     __ballot_sync / __shfl_sync (the warp-cooperative compare of
                                     north_star); default: one thread per read.  Same results. */
 
+#define SA_MATCH_SMEM_TREE 64u /* the shared-memory top tree: with an `order`
+                                   from sa_match_order, each CTA of 256 reads stages the records of the
+                                   first L levels of the binary search over its reads' SA range into
+                                   shared memory (one TMA bulk copy per record) and every read walks them
+                                   before its own probes.  L = SA_MATCH_TREE_LEVELS (1..12, 0 = 8); the
+                                   key length of the order = SA_MATCH_TREE_KEY_BASES (0 = 12).  Record
+                                   layouts, reads of <= 128 bases, no sub-tables.  Same results. */
+#define SA_MATCH_TREE_LEVELS(l) (((uint32_t)(l) & 15u) << 8)
+#define SA_MATCH_TREE_KEY_BASES(b) (((uint32_t)(b) & 31u) << 12)
+
 /* Build the index of ref_ascii[0..n) (host memory, case-insensitive ACGT) on
  * the device: validate + pack to 2 bits/base, build the suffix array on the
  * GPU (radix sort + prefix doubling), build the k-mer bracket table.
@@ -142,7 +152,8 @@ sa_status sa_index_export_text(const sa_index *idx, uint64_t *host_out);
  *             (Alg. 1 lines 44-45, res[thd<<1] = LB, res[(thd<<1)+1] = RB, reading A8).
  *   workspace dev scratch of sa_match_workspace_size(..., flags, ...) bytes (may be NULL if
  *             that is 0).  With SA_MATCH_STATS its first 4*Q bytes receive the statistics.
- *   flags     0, or SA_MATCH_STATS / SA_MATCH_PRESORT / SA_MATCH_ROWS_ORDERED / SA_MATCH_COOPERATIVE.
+ *   flags     0, or SA_MATCH_STATS / SA_MATCH_PRESORT / SA_MATCH_ROWS_ORDERED / SA_MATCH_COOPERATIVE /
+ *             SA_MATCH_SMEM_TREE (| SA_MATCH_TREE_LEVELS(l) | SA_MATCH_TREE_KEY_BASES(b)).
  * Requirements: every length m <= 32*stride_words (longer lengths are clamped) and
  * m <= 65535; stride_words = 0 selects the dense layout (above).  Q == 0 is a no-op.
  * Errors: SA_EINVAL.  Asynchronous on `stream`. */
@@ -196,27 +207,44 @@ sa_status sa_locate(const sa_index *idx, const uint32_t *out_lohi, const uint64_
 sa_status sa_tool_random_gather(int32_t device, uint64_t buffer_bytes, uint32_t access_bytes, uint64_t n_threads,
                                 uint32_t loads, int32_t dependent, float *ms);
 
-/* Partitioned index: for references whose index exceeds one GPU, rank
- * `part` of `nparts` keeps only the reads' route range [part_keys[part], part_keys[part+1]) of the
- * first route_bases bases (route_bases < k): the SA ranks and bracket-table entries those reads can
- * touch, plus the whole packed text.  Boundaries balance the SA ranks over the parts.  (This version
- * builds the whole index on each rank first and then keeps its slice.)  A partition answers reads of
- * length >= k only (shorter ones get lo = hi = 0xFFFFFFFF); its intervals are global SA ranks.
- *   sa_index_part_info: part_keys receives nparts+1 route-key boundaries.
- *   sa_match_route:     orders a batch by route key (order, as sa_match_order), gathers the rows in that
- *                       order (ordered_words/_len, as SA_MATCH_ROWS_ORDERED) and writes dest_offsets
- *                       (dev, nparts+1 uint64): the reads for part g are ordered rows
- *                       [dest_offsets[g], dest_offsets[g+1]).  Workspace: sa_match_order_workspace_size.
+/* Partitioned index (not in the paper): for references whose index exceeds one
+ * GPU.  Part `part` of `nparts` (>= 2) holds the suffixes whose route key -- their first route_bases
+ * (1..12, < k) bases, a suffix shorter than that padded with 'a' and placed like the k-mer table does --
+ * lies in [part_keys[part], part_keys[part+1]): a contiguous range of SA ranks [rank_lo, rank_hi).
+ * Boundaries balance the ranks over the parts.  sa_index_create_part builds ONLY that slice of the suffix
+ * array (MSD refinement of the part's suffixes on the packed text), of the k-mer table (entries
+ * [part_keys[part], part_keys[part+1]] x 4^(k-route_bases), clamped to the slice's ranks) and of the
+ * records, plus the whole packed text and the route-level table (4^route_bases + 1 uint32); opts.flags may
+ * only choose the layout.  Every answer of a part is clamped to its ranks: [clamp(lo), clamp(hi)] with
+ * clamp(v) = min(max(v, rank_lo), rank_hi) -- the global interval for a read routed to the part (route
+ * key inside its range), and for a read shorter than route_bases (sent to every part) a term of
+ * lo = sum over parts of (clamp(lo) - rank_lo) (sa_part_collect).  sa_index_export_sa / _table copy the
+ * slice (rank_hi - rank_lo SA entries; the table entries of the part's route keys).
+ *   sa_index_part_info: part_keys / part_ranks (nullable) receive nparts+1 route-key / rank boundaries.
+ *   sa_match_route:     orders a batch by route key, reads shorter than route_bases last (order, as
+ *                       sa_match_order), gathers the rows in that order (ordered_words/_len) and writes
+ *                       dest_offsets (dev, nparts+1 uint64): ordered rows [dest_offsets[g], dest_offsets[g+1])
+ *                       are routed to part g; rows [dest_offsets[nparts], Q) are the short reads.
+ *                       Workspace: sa_match_order_workspace_size.
+ *   sa_part_pack:       the send buffer (dev, send_rows = dest_offsets[nparts] + nparts * n_short rows):
+ *                       block g = the rows routed to part g followed by all short rows.
+ *   sa_part_collect:    back_lohi (dev) = the parts' answers to the blocks, in the same layout (after the
+ *                       all-to-all back); writes every read's global interval to out_lohi at read order[t].
  *   sa_scatter_results: out_lohi[order[t]] = in_lohi[t] (results back in the batch's own order).
- * The exchange itself (an all-to-all of rows and of intervals) is the caller's collective
+ * The exchange itself (all-to-all of the rows and of the intervals) is the caller's collective
  * (paper_1303_3692_b200/shard.py: torch.distributed all_to_all_single over NCCL). */
 sa_status sa_index_create_part(const char *ref_ascii, uint64_t n, const sa_index_opts *opts, uint32_t part,
                                uint32_t nparts, uint32_t route_bases, sa_index **out);
 sa_status sa_index_part_info(const sa_index *idx, uint32_t *part, uint32_t *nparts, uint32_t *route_bases,
-                             uint64_t *rank_lo, uint64_t *rank_hi, uint32_t *part_keys);
+                             uint64_t *rank_lo, uint64_t *rank_hi, uint32_t *part_keys, uint64_t *part_ranks);
 sa_status sa_match_route(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                          uint32_t stride_words, uint64_t Q, uint32_t *order, uint64_t *ordered_words,
                          uint32_t *ordered_len, uint64_t *dest_offsets, void *workspace, size_t ws_bytes, void *stream);
+sa_status sa_part_pack(const sa_index *idx, const uint64_t *ordered_words, const uint32_t *ordered_len,
+                       uint32_t stride_words, const uint64_t *dest_offsets, uint64_t Q, uint64_t send_rows,
+                       uint64_t *send_words, uint32_t *send_len, void *stream);
+sa_status sa_part_collect(const sa_index *idx, const uint32_t *back_lohi, const uint64_t *dest_offsets, uint64_t Q,
+                          const uint32_t *order, uint32_t *out_lohi, void *stream);
 sa_status sa_scatter_results(const uint32_t *order, const uint32_t *in_lohi, uint64_t Q, uint32_t *out_lohi,
                              void *stream);
 

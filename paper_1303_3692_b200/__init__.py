@@ -27,6 +27,7 @@ SA_MATCH_STATS = 1          # sa_match_batch flags: per-query steps | text windo
 SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 12 bases before the search
 SA_MATCH_ROWS_ORDERED = 8   # sa_match_batch flags: rows already arranged in `order` order
 SA_MATCH_COOPERATIVE = 32   # sa_match_batch flags: reads over 128 bases searched by 8/16/32-lane groups
+SA_MATCH_SMEM_TREE = 64     # sa_match_batch flags: shared-memory top tree per CTA (needs an order)
 SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 SA_INDEX_SUBTABLE = 8       # sa_index_opts.flags: (k+4)-base sub-tables for buckets of > 32 suffixes
 LAYOUTS = {"rec16": 0, "rec32": SA_INDEX_REC32, "plain": SA_INDEX_PLAIN}
@@ -62,8 +63,10 @@ _SIGS = {
     "sa_dc3_trace": ([_p, _u64, _p, _p], ctypes.c_int),
     "sa_index_create_part": ([_p, _u64, ctypes.POINTER(_Opts), _u32, _u32, _u32, ctypes.POINTER(_p)], ctypes.c_int),
     "sa_index_part_info": ([_p, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32),
-                            ctypes.POINTER(_u64), ctypes.POINTER(_u64), _p], ctypes.c_int),
+                            ctypes.POINTER(_u64), ctypes.POINTER(_u64), _p, _p], ctypes.c_int),
     "sa_match_route": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
+    "sa_part_pack": ([_p, _p, _p, _u32, _p, _u64, _u64, _p, _p, _p], ctypes.c_int),
+    "sa_part_collect": ([_p, _p, _p, _u64, _p, _p, _p], ctypes.c_int),
     "sa_scatter_results": ([_p, _p, _u64, _p, _p], ctypes.c_int),
     "sa_tree_create": ([_p, ctypes.POINTER(_p)], ctypes.c_int),
     "sa_tree_destroy": ([_p], None),
@@ -164,6 +167,7 @@ class Index:
             _check(lib().sa_index_create_part(ptr, arr.size, ctypes.byref(opts), int(part[0]), int(part[1]),
                                               int(part[2]), ctypes.byref(h)), "sa_index_create_part")
         self._h = h
+        self._part = part is not None
         n, kk, nb, dev = _u64(), _u32(), _u64(), _i32()
         _check(lib().sa_index_info(h, ctypes.byref(n), ctypes.byref(kk), ctypes.byref(nb), ctypes.byref(dev)),
                "sa_index_info")
@@ -172,14 +176,18 @@ class Index:
     def part_info(self) -> dict:
         p, np_, rb, lo, hi = _u32(), _u32(), _u32(), _u64(), _u64()
         _check(lib().sa_index_part_info(self._h, ctypes.byref(p), ctypes.byref(np_), ctypes.byref(rb),
-                                        ctypes.byref(lo), ctypes.byref(hi), None), "sa_index_part_info")
+                                        ctypes.byref(lo), ctypes.byref(hi), None, None), "sa_index_part_info")
         keys = np.empty(np_.value + 1, dtype=np.uint32)
-        _check(lib().sa_index_part_info(self._h, None, None, None, None, None, keys.ctypes.data), "sa_index_part_info")
+        ranks = np.empty(np_.value + 1, dtype=np.uint64)
+        _check(lib().sa_index_part_info(self._h, None, None, None, None, None, keys.ctypes.data, ranks.ctypes.data),
+               "sa_index_part_info")
         return {"part": p.value, "nparts": np_.value, "route_bases": rb.value, "rank_lo": lo.value,
-                "rank_hi": hi.value, "part_keys": keys.tolist()}
+                "rank_hi": hi.value, "part_keys": keys.tolist(), "part_ranks": ranks.tolist()}
 
     def route(self, words, lens=None, fixed_len: Optional[int] = None, stream=None):
-        """sa_match_route: (order int32[Q], ordered words, ordered lens or None, dest offsets int64[nparts+1])."""
+        """sa_match_route: (order int32[Q], ordered words, ordered lens or None, dest offsets int64[nparts+1]);
+        ordered rows [offs[g], offs[g+1]) go to part g, rows [offs[nparts], Q) (reads shorter than the route key)
+        to every part."""
         import torch
         Q, stride = words.shape
         need = _sz()
@@ -194,6 +202,25 @@ class Index:
                                     _dptr(ow), _dptr(ol), _dptr(offs), _dptr(ws), need.value, _stream_ptr(stream)),
                "sa_match_route")
         return order, ow, ol, offs
+
+    def part_pack(self, ordered_words, ordered_lens, offs, send_rows: int, stream=None):
+        """sa_part_pack: the all-to-all send buffer (block g = rows routed to part g + all short rows)."""
+        import torch
+        Q, stride = ordered_words.shape
+        sw = _empty((send_rows, stride), ordered_words.dtype, ordered_words.device, stream)
+        sl = None if ordered_lens is None else _empty(send_rows, ordered_lens.dtype, ordered_lens.device, stream)
+        _check(lib().sa_part_pack(self._h, _dptr(ordered_words), _dptr(ordered_lens), stride, _dptr(offs), Q, send_rows,
+                                  _dptr(sw), _dptr(sl), _stream_ptr(stream)), "sa_part_pack")
+        return sw, sl
+
+    def part_collect(self, back, offs, order, Q: int, out=None, stream=None):
+        """sa_part_collect: every read's global interval from the parts' answers, at the read's own index."""
+        import torch
+        if out is None:
+            out = _empty((Q, 2), torch.int32, back.device, stream)
+        _check(lib().sa_part_collect(self._h, _dptr(back), _dptr(offs), Q, _dptr(order), _dptr(out),
+                                     _stream_ptr(stream)), "sa_part_collect")
+        return out
 
     # ---- lifetime ----
     def close(self):
@@ -214,13 +241,24 @@ class Index:
         self.close()
 
     # ---- exports (for checking against the oracle) ----
+    def _slice(self):
+        """(SA entries, table entries) held by this index: all of them, or a partition's slice."""
+        if not getattr(self, "_part", None):
+            return self.n, (1 << (2 * self.k)) + 1
+        pi = self.part_info()
+        g, rb = pi["part"], pi["route_bases"]
+        keys = pi["part_keys"]
+        return pi["rank_hi"] - pi["rank_lo"], (keys[g + 1] - keys[g]) * (1 << (2 * (self.k - rb))) + 1
+
     def export_sa(self) -> np.ndarray:
-        out = np.empty(self.n, dtype=np.uint32)
+        """The suffix array (a partition: its slice SA[rank_lo .. rank_hi))."""
+        out = np.empty(self._slice()[0], dtype=np.uint32)
         _check(lib().sa_index_export_sa(self._h, out.ctypes.data), "sa_index_export_sa")
         return out
 
     def export_table(self) -> np.ndarray:
-        out = np.empty((1 << (2 * self.k)) + 1, dtype=np.uint32)
+        """The k-mer bracket table (a partition: the entries of its route keys, clamped to its ranks)."""
+        out = np.empty(self._slice()[1], dtype=np.uint32)
         _check(lib().sa_index_export_table(self._h, out.ctypes.data), "sa_index_export_table")
         return out
 
@@ -260,7 +298,7 @@ class Index:
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
               presort: bool = False, workspace=None, order=None, rows_ordered: bool = False,
-              n_reads: Optional[int] = None, cooperative: bool = False):
+              n_reads: Optional[int] = None, cooperative: bool = False, smem_tree: int = 0, tree_key_bases: int = 0):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
@@ -270,6 +308,7 @@ class Index:
         rows_ordered: words/lens are order()'s ordered_words/ordered_lens (row t is read order[t]).
         n_reads: with a 1-D `words` stream and fixed_len: the dense layout (include/sa.h).
         cooperative: SA_MATCH_COOPERATIVE (reads over 128 bases: 8/16/32 lanes per read).
+        smem_tree: L > 0 selects SA_MATCH_SMEM_TREE with L levels (tree_key_bases: the order's key length).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [2, Q]: row 0 steps | text windows << 16, row 1 the
@@ -287,6 +326,8 @@ class Index:
         assert out.is_cuda and out.dtype == torch.int32 and out.numel() == 2 * Q and out.is_contiguous()
         flags = (SA_MATCH_STATS if want_stats else 0) | (SA_MATCH_PRESORT if presort else 0) | \
                 (SA_MATCH_ROWS_ORDERED if rows_ordered else 0) | (SA_MATCH_COOPERATIVE if cooperative else 0)
+        if smem_tree:  # levels of the shared-memory top tree (include/sa.h SA_MATCH_SMEM_TREE)
+            flags |= SA_MATCH_SMEM_TREE | ((int(smem_tree) & 15) << 8) | ((int(tree_key_bases) & 31) << 12)
         need = self.workspace_size(Q, stride, flags) \
             if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
         if need and (workspace is None or workspace.numel() < need):

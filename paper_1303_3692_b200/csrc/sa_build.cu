@@ -129,12 +129,7 @@ struct MaxU32 {
 // along the SA, and T[x] = #{r : e(r) < x} = r for e(r-1) < x <= e(r).
 __device__ __forceinline__ int64_t kmer_e(const uint64_t *__restrict__ text, uint64_t n, const uint32_t *__restrict__ sa,
                                           uint64_t r, unsigned k) {
-    const uint64_t s = sa[r];
-    const uint64_t len = n - s;
-    uint64_t w = text_window(text, s);
-    if (len < k) w &= prefix_mask((unsigned)len);
-    const int64_t code = (int64_t)(w >> (64 - 2 * k));
-    return len >= k ? code : code - 1;
+    return sa_suffix_e(text, n, sa[r], k);
 }
 
 __global__ void k_table(const uint64_t *__restrict__ text, uint64_t n, const uint32_t *__restrict__ sa, unsigned k,
@@ -336,8 +331,8 @@ sa_status build_sa(sa_index *idx, cudaStream_t st) {
 //   L_REC16: {SA[r], bases k+32..k+47 (high half), bases k..k+31 (lo, hi)}
 //   L_REC32: {SA[r], bases k+96..k+111 (high half), bases k..k+31 (lo, hi)}, {k+32..k+63, k+64..k+95}
 __global__ void k_records(const uint64_t *__restrict__ text, uint64_t n, unsigned k, const uint32_t *__restrict__ sa,
-                          uint4 *__restrict__ rec, int wide) {
-    GRID_STRIDE(r, n) {
+                          uint4 *__restrict__ rec, int wide, uint64_t count) {
+    GRID_STRIDE(r, count) {
         const uint64_t s = sa[r];
         const uint64_t c0 = text_window(text, s + k);
         if (!wide) {
@@ -360,7 +355,7 @@ __global__ void k_extract_sa(const uint4 *__restrict__ rec, uint64_t count, unsi
 }  // namespace
 
 sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out) {
-    const uint64_t n = idx->n;
+    const uint64_t n = idx->nparts > 1 ? idx->rank_end - idx->rank_base : idx->n;  // a partition: its slice
     if (idx->layout == 0) {
         SA_CUDA_TRY(cudaMemcpy(host_out, idx->sa, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
         return SA_OK;
@@ -375,6 +370,22 @@ sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out) {
         SA_CUDA_TRY(cudaGetLastError());
         SA_CUDA_TRY(cudaMemcpy(host_out + off, tmp.p, c * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     }
+    return SA_OK;
+}
+
+// idx->rec = the records of the `count` suffixes sa[0..count) (layout 1 or 2); trims the memory pool
+// first so the records can take the build's transient memory.
+sa_status sa_build_records(sa_index *idx, const uint32_t *sa, uint64_t count, cudaStream_t st) {
+    const uint64_t per = idx->layout == 2 ? 2 : 1;
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    SA_CUDA_TRY(cudaMalloc(&idx->rec, (count ? count : 1) * per * sizeof(uint4)));
+    if (count) {
+        k_records<<<grid_for(count), kThreads, 0, st>>>(idx->text, idx->n, idx->k, sa, idx->rec, per == 2, count);
+        SA_CUDA_TRY(cudaGetLastError());
+    }
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
     return SA_OK;
 }
 
@@ -419,6 +430,7 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
     // ---- 3. k-mer bracket table ----
     const uint64_t K = 1ull << (2 * idx->k);
     SA_CUDA_TRY(cudaMalloc(&idx->table, (K + 1) * sizeof(uint32_t)));
+    idx->table_entries = K + 1;
     k_table<<<grid_for(n + 1), kThreads, 0, st>>>(idx->text, n, idx->sa, idx->k, idx->table);
     SA_CUDA_TRY(cudaGetLastError());
     // ---- 3b. second-level tables for the large buckets (SA_INDEX_SUBTABLE) ----
@@ -473,17 +485,10 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
     // ---- 4. SA records (default layout) ----
     uint64_t sa_bytes = n * sizeof(uint32_t);
     if (idx->layout != 0) {
-        const uint64_t per = idx->layout == 2 ? 2 : 1;
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-        SA_CUDA_TRY(cudaMalloc(&idx->rec, n * per * sizeof(uint4)));
-        k_records<<<grid_for(n), kThreads, 0, st>>>(idx->text, n, idx->k, idx->sa, idx->rec, per == 2);
-        SA_CUDA_TRY(cudaGetLastError());
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(sa_build_records(idx, idx->sa, n, st));
         SA_CUDA_TRY(cudaFree(idx->sa));
         idx->sa = nullptr;
-        sa_bytes = n * per * sizeof(uint4);
+        sa_bytes = n * (idx->layout == 2 ? 2 : 1) * sizeof(uint4);
     }
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     idx->device_bytes = idx->n_words * 8 + sa_bytes + (K + 1) * 4 + idx->big_count * 257 * 4 +

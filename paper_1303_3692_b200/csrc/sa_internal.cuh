@@ -99,12 +99,18 @@ struct sa_index {
     uint32_t big_bits = 0;       // log2 of the hash table size
     unsigned long long *big_hash = nullptr;  // dev: open addressing, x << 32 | sub-table id, empty = kBigEmpty
     uint32_t *big_sub = nullptr; // dev: big_count x 257 global SA ranks
-    // partitioned index (sa_index_create_part): this index holds SA ranks [rank_base, rank_end) and
-    // table entries [x_base, x_end] only, i.e. the reads whose first route_bases bases lie in
-    // [part_keys[part], part_keys[part+1])
+    // partitioned index (sa_index_create_part, csrc/sa_part.cu): this index holds SA ranks
+    // [rank_base, rank_end) and table entries [x_base, x_base + 4^(k-rb) * (keys in the part)] only:
+    // the suffixes whose route key (first route_bases bases, sa_suffix_e) lies in
+    // [part_keys[part], part_keys[part+1]); part_ranks[g] = first rank of part g (all parts);
+    // route_table = the route-level bracket table T_r[K] = #{i : trunc_rb(S_i) < K}, K in [0, 4^rb]
     uint32_t part = 0, nparts = 1, route_bases = 0;
     uint64_t x_base = 0, rank_base = 0, rank_end = 0;
     std::vector<uint32_t> part_keys;
+    std::vector<uint64_t> part_ranks;
+    uint64_t table_entries = 0;          // entries of `table` (a partition: its slice)
+    uint32_t *route_table = nullptr;     // dev
+    uint64_t *part_ranks_dev = nullptr;  // dev copy of part_ranks
     // host-buffer pipeline (sa_match_batch_host); grown on demand, guarded by mu
     std::mutex mu;
     cudaStream_t pipe_stream[2] = {nullptr, nullptr};
@@ -178,6 +184,16 @@ __device__ __forceinline__ uint32_t reload_u32(const uint32_t *p) {
     return v;
 }
 
+// TMA bulk prefetch of global bytes [p, p + bytes) into L2 (cp.async.bulk.prefetch.L2: one instruction,
+// no registers, no completion to wait for); the range is widened to 16-byte granules as the
+// instruction requires.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint64_t bytes) {
+    const uint64_t a = reinterpret_cast<uint64_t>(p);
+    const uint64_t lo = a & ~15ull, hi = (a + bytes + 15) & ~15ull;
+    if (hi > lo)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+}
+
 // 32 bases of the packed text starting at base b (b < n + 32); bases past n read as 0 ('a').
 __device__ __forceinline__ uint64_t text_window(const uint64_t *__restrict__ text, uint64_t b) {
     const uint64_t w = b >> 5;
@@ -192,6 +208,17 @@ __device__ __forceinline__ uint64_t prefix_mask(unsigned L) {
     return L >= 32 ? ~0ull : (L == 0 ? 0ull : ~(~0ull >> (2u * L)));
 }
 
+// e_j(s): the j-mer code of suffix s when it has >= j bases; U - 1 for a shorter suffix whose a-padded
+// j-mer is U.  e is non-decreasing along the SA, and #{i : e_j(i) < x} = #{i : trunc_j(S_i) < x}: the
+// bracket table T[x] counts the suffixes with e < x (k_table).
+__device__ __forceinline__ int64_t sa_suffix_e(const uint64_t *__restrict__ text, uint64_t n, uint64_t s, unsigned j) {
+    const uint64_t len = n - s;
+    uint64_t w = text_window(text, s);
+    if (len < j) w &= prefix_mask((unsigned)len);
+    const int64_t code = (int64_t)(w >> (64 - 2 * j));
+    return len >= j ? code : code - 1;
+}
+
 // (for a partition the base is shifted so that global SA ranks index it)
 inline SaView sa_view(const sa_index *idx) {
     if (idx->layout == 0) return SaView{idx->sa - idx->rank_base, 1u};
@@ -204,3 +231,5 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st);
 sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out);
 sa_status sa_pack_text(sa_index *idx, const char *ref_ascii, cudaStream_t st);
 sa_status sa_build_sa_dc3(sa_index *idx, cudaStream_t st, uint32_t *trace_rank, uint32_t *trace_nonsample);
+sa_status sa_build_records(sa_index *idx, const uint32_t *sa, uint64_t count, cudaStream_t st);
+void sa_free_index(sa_index *idx);

@@ -33,6 +33,22 @@ cudaError_t launch_g(const MatchArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int QW>
+cudaError_t launch_tree(const MatchArgs &a, int layout, uint32_t levels, uint32_t key_bases, cudaStream_t st) {
+    using namespace sa_search;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+    const size_t smem = (size_t)((1u << levels) - 1) * (layout == L_REC32 ? 32 : 16);
+    if (layout == L_REC32) {
+        cudaFuncSetAttribute(k_match_tree<QW, L_REC32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_match_tree<QW, L_REC32><<<blocks, threads, smem, st>>>(a, levels, key_bases);
+    } else {
+        cudaFuncSetAttribute(k_match_tree<QW, L_REC16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_match_tree<QW, L_REC16><<<blocks, threads, smem, st>>>(a, levels, key_bases);
+    }
+    return cudaGetLastError();
+}
+
 template <int G, int WPL>
 cudaError_t launch_group(const MatchArgs &a, int layout, bool stats, cudaStream_t st) {
     using namespace sa_search;
@@ -55,9 +71,12 @@ cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t s
 
 // ---- presort (SA_MATCH_PRESORT) ---------------------------------------------------------------
 // key = the read's first 16 bases (masked to its length), value = read index
+// (short_last: a read shorter than key_bases gets the key 4^key_bases, after every full key -- the
+// routing of a partitioned index sends those reads to every part)
 __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens,
                                uint32_t fixed_len, uint32_t stride, uint64_t dense_words, uint64_t Q,
-                               uint32_t key_bases, uint32_t *__restrict__ keys, uint32_t *__restrict__ perm) {
+                               uint32_t key_bases, bool short_last, uint32_t *__restrict__ keys,
+                               uint32_t *__restrict__ perm) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t m;
         uint64_t w0;
@@ -73,7 +92,7 @@ __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_
             w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
         }
         const uint32_t pre = (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases));
-        keys[q] = pre;
+        keys[q] = (short_last && m < key_bases) ? (1u << (2 * key_bases)) : pre;
         perm[q] = (uint32_t)q;
     }
 }
@@ -128,7 +147,8 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
 constexpr uint32_t kDefaultKeyBases = 12;
 
 sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len, uint32_t stride, uint64_t Q,
-                      uint32_t key_bases, uint8_t *ws, const PresortLayout &L, uint32_t *order, cudaStream_t st) {
+                      uint32_t key_bases, uint8_t *ws, const PresortLayout &L, uint32_t *order, cudaStream_t st,
+                      bool short_last = false) {
     uint32_t *keys_in = reinterpret_cast<uint32_t *>(ws + L.keys_in);
     uint32_t *keys_out = reinterpret_cast<uint32_t *>(ws + L.keys_out);
     uint32_t *perm_in = reinterpret_cast<uint32_t *>(ws + L.perm_in);
@@ -136,7 +156,7 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     const uint64_t dense_words = (Q * (uint64_t)fixed_len + 31) / 32;
     k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
-                                                     keys_in, perm_in);
+                                                     short_last, keys_in, perm_in);
     SA_CUDA_TRY(cudaGetLastError());
     size_t b = L.cub_bytes;
     // key = the first key_bases bases: ceil(2*key_bases/8) radix passes.  Measured and dropped
@@ -144,7 +164,7 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     // hand-written two-pass stable LSD counting sort with 10-12-bit digits +6.5-8.5 ms (its scattered
     // 4-byte stores are partial-sector DRAM read-modify-writes: 5.6 GB written, 5.2 GB read per pass
     // for 0.8 GB of payload; CUB's 8-bit digits keep each bin's run long enough to coalesce).
-    const int end_bit = 2 * (int)key_bases;
+    const int end_bit = 2 * (int)key_bases + (short_last ? 1 : 0);
     SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0,
                                                 end_bit, st));
     return SA_OK;
@@ -317,7 +337,7 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                               uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *order,
-                              bool rows_ordered, cudaStream_t st, bool cooperative = false) {
+                              bool rows_ordered, cudaStream_t st, bool cooperative = false, uint32_t tree_flags = 0) {
     MatchArgs a;
     a.rows_ordered = rows_ordered;
 
@@ -335,17 +355,24 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.out = out;
     a.stats = stats;
     a.order = order;
-    a.min_len = 0;
     a.big_hash = idx->big_hash;
     a.big_sub = idx->big_sub;
     a.big_bits = idx->big_bits;
+    a.clo = 0;
+    a.chi = (uint32_t)idx->n;
+    a.route = nullptr;
+    a.route_bases = 0;
     if (idx->nparts > 1) {
-        // a partition holds table entries [x_base, x_end] and SA ranks [rank_base, rank_end): address them
-        // with their global indices through shifted base pointers (only in-slice indices are dereferenced)
+        // a partition holds table entries [x_base, x_base + table_entries) and SA ranks [rank_base, rank_end):
+        // address them with their global indices through shifted base pointers; every bracket is clamped
+        // to the slice, so only in-slice indices are dereferenced (csrc/sa_part.cu)
         a.table = idx->table - idx->x_base;
         if (idx->layout == 0) a.sa = idx->sa - idx->rank_base;
         else a.rec = idx->rec - idx->rank_base * (idx->layout == 2 ? 2 : 1);
-        a.min_len = idx->k;
+        a.clo = (uint32_t)idx->rank_base;
+        a.chi = (uint32_t)idx->rank_end;
+        a.route = idx->route_table;
+        a.route_bases = idx->route_bases;
     }
     // one vector load per read row when the row is exactly QW words and suitably aligned
     const uintptr_t wp = reinterpret_cast<uintptr_t>(q_words);
@@ -356,6 +383,21 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     const bool st_on = stats != nullptr;
     const uint32_t nw = stride ? stride : (fixed_len + 31) / 32;  // register words needed
     cudaError_t e;
+    if (tree_flags & SA_MATCH_SMEM_TREE) {
+        uint32_t levels = (tree_flags >> 8) & 15, kb = (tree_flags >> 12) & 31;
+        if (levels == 0) levels = 8;
+        if (kb == 0) kb = kDefaultKeyBases;
+        if (idx->layout == 0 || nw > 4 || levels > 12 || kb > 16 || !order || idx->big_sub) {
+            sa_set_error("SA_MATCH_SMEM_TREE: needs a record layout, reads of <= 128 bases, an order, levels <= 12, "
+                         "key bases <= 16, no sub-tables");
+            return SA_EINVAL;
+        }
+        if (nw <= 1) e = launch_tree<1>(a, idx->layout, levels, kb, st);
+        else if (nw <= 2) e = launch_tree<2>(a, idx->layout, levels, kb, st);
+        else e = launch_tree<4>(a, idx->layout, levels, kb, st);
+        if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+        return SA_OK;
+    }
     // reads of more than 4 words: one thread per read, words from global memory; with
     // SA_MATCH_COOPERATIVE G = 8 / 16 / 32 lanes per read (measured slower)
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
@@ -377,7 +419,8 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
                                     void *stream) {
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
-    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED | SA_MATCH_COOPERATIVE)) {
+    if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED | SA_MATCH_COOPERATIVE | SA_MATCH_SMEM_TREE |
+                  0x1FF00u)) {
         sa_set_error("unknown flags 0x%x", flags);
         return SA_EINVAL;
     }
@@ -404,7 +447,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         return SA_EINVAL;
     }
     return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st,
-                        (flags & SA_MATCH_COOPERATIVE) != 0);
+                        (flags & SA_MATCH_COOPERATIVE) != 0, flags & (SA_MATCH_SMEM_TREE | 0x1FF00u));
 }
 
 // Synchronises the host pipeline's streams when sa_match_batch_host returns, on success and on every
@@ -478,12 +521,17 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
             SA_CUDA_TRY(cudaMemcpyAsync(idx->pipe_lens[b], q_len + q0, cq * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             dl = idx->pipe_lens[b];
         }
+#ifndef SA_HOST_NO_ORDER  // (A/B build: chunks matched in input order)
         PresortLayout L;
         SA_TRY(presort_layout(cq, false, true, true, L));
         SA_TRY(order_reads(idx->pipe_words[b], dl, fixed_len, stride, cq, kDefaultKeyBases,
                            static_cast<uint8_t *>(idx->pipe_ws[b]), L, idx->pipe_order[b], st));
-        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr,
-                            idx->pipe_order[b], false, st));
+        const uint32_t *ord = idx->pipe_order[b];
+#else
+        const uint32_t *ord = nullptr;
+#endif
+        SA_TRY(match_launch(idx, idx->pipe_words[b], dl, fixed_len, stride, cq, idx->pipe_out[b], nullptr, ord, false,
+                            st));
         SA_CUDA_TRY(cudaMemcpyAsync(out_lohi + 2 * q0, idx->pipe_out[b], cq * 2 * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, st));
     }
@@ -517,7 +565,7 @@ extern "C" sa_status sa_match_route(const sa_index *idx, const uint64_t *q_words
         return SA_EINVAL;
     }
     uint8_t *ws = static_cast<uint8_t *>(workspace);
-    SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, idx->route_bases, ws, L, order, st));
+    SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, idx->route_bases, ws, L, order, st, true));
     uint64_t blocks = (Q + 255) / 256;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     const bool vec = stride_words == 4 && (reinterpret_cast<uintptr_t>(q_words) & 31) == 0 &&

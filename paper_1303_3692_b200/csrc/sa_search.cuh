@@ -40,7 +40,11 @@ struct MatchArgs {
     bool vec_rows;                      // read rows can be loaded with one vector load (aligned, stride == QW)
     uint64_t dense_words;               // stride == 0: dense layout, words = one 2-bit stream of this many words
     bool rows_ordered;                  // SA_MATCH_ROWS_ORDERED: row t is read order[t]
-    uint32_t min_len;                   // partitioned index: reads shorter than k get (~0, ~0)
+    // the index's SA ranks [clo, chi): [0, n) for a whole index; a partition's slice (csrc/sa_part.cu),
+    // every bracket is clamped to it, so a read is answered as clamp(lo), clamp(hi)
+    uint32_t clo, chi;
+    const uint32_t *__restrict__ route;  // partition: route-level table T_r (4^rb + 1 entries), else NULL
+    uint32_t route_bases;                // partition: rb (reads with m < rb use T_r), else 0
     const unsigned long long *__restrict__ big_hash; // SA_INDEX_SUBTABLE: x << 32 | sub-table id, empty = ~0
     const uint32_t *__restrict__ big_sub;
     uint32_t big_bits;
@@ -138,6 +142,13 @@ struct QueryWords<0> {
         for (int u = 0; u < 4; ++u) w[u] = gword(4 * c + u);
     }
     __device__ __forceinline__ uint64_t first() const { return h[0]; }
+    // words j .. nw-1 of the row into L2 (TMA bulk prefetch)
+    __device__ __forceinline__ void prefetch_rows(uint32_t j) const {
+        if (j < nw) {
+            const uint64_t last = sh ? nw : nw - 1;  // (dense: one more word for the shift)
+            if (j < left) bulk_prefetch_l2(p + j, ((last < left ? last : left - 1) + 1 - j) * 8);
+        }
+    }
 };
 
 // ---- compare against the packed text --------------------------------------------------------
@@ -233,8 +244,25 @@ __device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, 
             return;
         }
         // 4 words per step: the read chunk and four text windows are loaded together (vector loads),
-        // so a long verification is ~m/128 dependent round trips instead of ~m/32
+        // so a long verification is ~m/128 dependent round trips instead of ~m/32.  (SA_BULK_PREFETCH:
+        // once 128 bases are known equal, the rest of the text window and of the read row are brought
+        // into L2 by one TMA bulk prefetch each -- measured slower, kept as an A/B build.)
+        bool fetched = false;
+        auto prefetch_rest = [&](uint32_t jfrom) {
+            if (fetched) return;
+            fetched = true;
+            const uint64_t b0 = s + 32ull * jfrom;                  // first base still to compare
+            const uint64_t b1 = s + (m < slen ? (uint64_t)m : slen);  // past the last one
+            if (b1 > b0) bulk_prefetch_l2(text + (b0 >> 5), (((b1 + 31) >> 5) + 1 - (b0 >> 5)) * 8);
+            P.prefetch_rows(jfrom);
+        };
+#ifdef SA_BULK_PREFETCH  // A/B build only: measured slower (r02b: m = 500 +18%, m = 1000 +7%)
+        if (j0 >= 4) prefetch_rest(j0);
+#endif
         for (uint32_t c = j0 >> 2; 4 * c < nw; ++c) {
+#ifdef SA_BULK_PREFETCH
+            if (4 * c > j0) prefetch_rest(4 * c);
+#endif
             uint64_t pw[4], tw[4] = {0, 0, 0, 0};
             P.chunk(c, pw);
             if (128ull * c < slen) text_windows4(text, s + 128ull * c, tw);
@@ -257,8 +285,26 @@ template <int L>
 struct Rec {
     static constexpr int kWords = (L == L_REC32) ? 4 : 2;             // 64-bit cache words
     static constexpr uint32_t kBases = (L == L_REC32) ? 112u : 48u;   // cached bases
+    static constexpr int kU4 = (L == L_REC32) ? 2 : 1;                 // uint4 per record
     uint32_t sa;
     uint64_t c[kWords];  // c[j] = bases k+32j .. k+32j+31 (the last word holds 16)
+    // a record staged in shared memory (k_match_tree)
+    __device__ __forceinline__ void load_shared(const uint4 *s) {
+        if constexpr (L == L_REC32) {
+            const ulonglong2 x = reinterpret_cast<const ulonglong2 *>(s)[0];
+            const ulonglong2 y = reinterpret_cast<const ulonglong2 *>(s)[1];
+            sa = (uint32_t)x.x;
+            c[0] = x.y;
+            c[1] = y.x;
+            c[2] = y.y;
+            c[3] = x.x & 0xFFFFFFFF00000000ull;
+        } else {
+            const uint4 v = s[0];
+            sa = v.x;
+            c[0] = ((uint64_t)v.w << 32) | v.z;
+            c[1] = (uint64_t)v.y << 32;
+        }
+    }
     __device__ __forceinline__ void load(const uint4 *__restrict__ rec, uint64_t p) {
         if constexpr (L == L_REC32) {
             uint64_t w0, w1, w2, w3;
@@ -566,31 +612,78 @@ __device__ __forceinline__ uint32_t bound(const MatchArgs &a, const RD &P, uint3
     return R;
 }
 
-// One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.
+// ---- the shared-memory top tree (SA_MATCH_SMEM_TREE, k_match_tree) ----------------------------
+// The first `levels` levels of the binary search over a CTA's rank range (Lp1 - 1, R): BFS node i
+// (1-based) holds the record of its pivot, staged in shared memory by TMA bulk copies.
+struct TreeCtx {
+    const uint4 *nodes;   // shared: node i at nodes[(i - 1) * kU4]
+    uint32_t Lp1, R;      // the root's range
+    uint32_t levels;
+};
+
+// Walk the tree with the read's own search state (Lp1 - 1, R): a node's pivot inside that interval is
+// a probe that costs no DRAM access; the walk follows the side that still holds the interval.  Returns
+// true at the split (P a prefix of the pivot's suffix), with the RB search's start state set.
 template <int L, class RD>
+__device__ __forceinline__ bool tree_descent(const MatchArgs &a, const TreeCtx &tc, const RD &P, uint32_t m,
+                                             uint32_t &Lp1, uint32_t &R, uint32_t &lcpL, uint32_t &lcpR,
+                                             uint32_t &hLp1, uint32_t &hR, uint32_t &hlcpL, uint32_t &hlcpR,
+                                             uint32_t &steps, uint32_t &texts) {
+    uint32_t tL = tc.Lp1, tR = tc.R, node = 1;
+    for (uint32_t d = 0; d < tc.levels && tR > tL; ++d) {
+        const uint32_t p = (uint32_t)(((uint64_t)tL - 1 + tR) >> 1);
+        if (p >= Lp1 && p < R) {
+            Probe<L> pr;
+            pr.r.load_shared(tc.nodes + (uint64_t)(node - 1) * Rec<L>::kU4);
+            int sign;
+            uint32_t lcp;
+            compare_probe(a, pr, P, m, min(lcpL, lcpR), true, sign, lcp, texts);
+            ++steps;
+            if (sign == 0) {
+                hLp1 = p + 1; hR = R; hlcpL = lcp; hlcpR = lcpR;
+                R = p; lcpR = lcp;
+                return true;
+            }
+            if (sign < 0) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+        }
+        if (R <= p) { tR = p; node = 2 * node; } else { tL = p + 1; node = 2 * node + 1; }
+    }
+    return false;
+}
+
+// One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.
+template <int L, bool TREE = false, class RD>
 __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uint32_t m, uint32_t &lo,
-                                            uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes) {
+                                            uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
+                                            const TreeCtx *tc = nullptr) {
     const uint32_t k = a.k;
-    if (m == 0) {  // the empty read is a prefix of every suffix (reading A12)
-        lo = 0;
-        hi = (uint32_t)a.n;
+    auto clamp = [&](uint32_t v) { return min(max(v, a.clo), a.chi); };
+    if (m == 0) {  // the empty read is a prefix of every suffix (reading A12): [0, n), clamped
+        lo = a.clo;
+        hi = a.chi;
         return;
     }
     if (m < k) {
         // lo in [T[xa]-(k-m), T[xa]], hi in [T[xb]-(k-1), T[xb]], xa = x.a^(k-m), xb = (x+1).a^(k-m)
-        // (DESIGN.md "Bracket, short reads"); each searched over (T[.]-k-1, T[.])
+        // (DESIGN.md "Bracket, short reads"); each searched over (T[.]-k-1, T[.]).  A partition answers a
+        // read shorter than its route key with the route-level table T_r (the same rule at rb bases).
+        const bool rt = m < a.route_bases;
+        const uint32_t kk = rt ? a.route_bases : k;
+        const uint32_t *T = rt ? a.route : a.table;
         const uint64_t x = P.first() >> (64 - 2 * m);
-        const uint32_t Ta = ld_u32(a.table + (x << (2 * (k - m))));
-        const uint32_t Tb = ld_u32(a.table + ((x + 1) << (2 * (k - m))));
+        const uint32_t Ta = ld_u32(T + (x << (2 * (kk - m))));
+        const uint32_t Tb = ld_u32(T + ((x + 1) << (2 * (kk - m))));
         ubytes += 8;  // the two table entries
-        lo = bound<L>(a, P, m, Ta > k ? Ta - k : 0, Ta, 0, 0, true, false, steps, texts, ubytes);
-        hi = bound<L>(a, P, m, Tb > k ? Tb - k : 0, Tb, 0, 0, false, false, steps, texts, ubytes);
+        lo = bound<L>(a, P, m, clamp(Ta > kk ? Ta - kk : 0), clamp(Ta), 0, 0, true, false, steps, texts, ubytes);
+        hi = bound<L>(a, P, m, clamp(Tb > kk ? Tb - kk : 0), clamp(Tb), 0, 0, false, false, steps, texts, ubytes);
         return;
     }
     // all suffixes before T[x] are < P, all from T[x+1] on are > P
     const uint64_t x = P.first() >> (64 - 2 * k);
     uint32_t Lp1, R;
     table_pair(a.table, x, Lp1, R);
+    Lp1 = clamp(Lp1);
+    R = clamp(R);
     ubytes += 8;  // T[x], T[x+1]
     if (a.big_sub && R - Lp1 > kBigBucket && m >= k + 4) {
         // a large bucket (repeats): its (k+4)-base sub-table narrows the bracket by the next 4 bases
@@ -611,7 +704,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
     uint32_t lcpL = 0, lcpR = 0;
     uint32_t hLp1 = 0, hR = 0, hlcpL = 0, hlcpR = 0;
     bool split = false;
-    while (R > Lp1) {  // LB rule until the first pivot where P is a prefix of the suffix (the split)
+    if constexpr (TREE) split = tree_descent<L>(a, *tc, P, m, Lp1, R, lcpL, lcpR, hLp1, hR, hlcpL, hlcpR, steps, texts);
+    while (!split && R > Lp1) {  // LB rule until the first pivot where P is a prefix of the suffix (the split)
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
@@ -664,8 +758,11 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 #ifndef SA_MATCH_MINB
 #define SA_MATCH_MINB (1280 / SA_MATCH_THREADS)
 #endif
-// (the long-read instantiation, QW = 0, keeps ptxas's own choice: capped it spills)
-#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS, QW > 0 ? SA_MATCH_MINB : 1)
+// (the long-read instantiation, QW = 0: 4 x 256 threads = 64 registers, the r01 build's allocation)
+#ifndef SA_MATCH_MINB_LONG
+#define SA_MATCH_MINB_LONG (1024 / SA_MATCH_THREADS)
+#endif
+#define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS, QW > 0 ? SA_MATCH_MINB : SA_MATCH_MINB_LONG)
 template <int QW, int L, bool STATS>
 __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -677,11 +774,7 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     load_read<QW>(a, row, m, P);
     // ubytes (SA_MATCH_STATS): the read (2 bits/base) + the 8-byte result + what the search adds
     uint32_t lo, hi, steps = 0, texts = 0, ubytes = ((m + 3) >> 2) + 8;
-    if (m < a.min_len) {  // a partition cannot answer a read shorter than k (its window may leave the slice)
-        lo = hi = 0xFFFFFFFFu;
-    } else {
-        search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
-    }
+    search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here.
     // The read index is loaded again here (an L1 hit) rather than kept live across the search: at the
     // 48 registers of the 62.5%-occupancy build ptxas otherwise spills it to local memory.
@@ -695,6 +788,100 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     if (STATS) {
         a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
         a.stats[a.Q + q] = ubytes;
+    }
+}
+
+// k_match with the shared-memory top tree (north_star's "top levels of the SA
+// binary-search tree staged in shared memory via TMA"; the B200 form of the paper's shared-memory
+// tiles).  The reads are ordered (sa_match_order by key_bases bases), so a CTA's 256
+// reads share one range of the suffix array: [T[first read's key], T[last read's key + 1]).  The
+// CTA stages the records of the first `levels` levels of the binary search over that range into
+// shared memory with one cp.async.bulk per record (mbarrier completion), and every read walks them
+// (tree_descent) before its own DRAM probes.
+template <int QW, int L>
+__global__ void __launch_bounds__(256, 4) k_match_tree(const MatchArgs a, uint32_t levels, uint32_t key_bases) {
+    extern __shared__ __align__(128) uint4 s_nodes[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_lo, s_hi;
+    constexpr uint32_t U4 = Rec<L>::kU4;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x;
+    const uint64_t t = t0 + threadIdx.x;
+    const uint32_t nodes = (1u << levels) - 1;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t k = a.k, kb = key_bases;
+    if (threadIdx.x == 0) {
+        // the ordering keys of the block's first and last read
+        auto key_of = [&](uint64_t slot) -> uint64_t {
+            const uint64_t q = a.order ? (uint64_t)__ldg(a.order + slot) : slot;
+            const uint64_t row = a.rows_ordered ? slot : q;
+            const uint32_t m = read_len(a, row);
+            uint64_t w0;
+            if (a.stride == 0) {
+                const uint64_t bit = 2ull * m * row, i = bit >> 6;
+                const unsigned sh = (unsigned)(bit & 63);
+                const uint64_t lo = ld_u64(a.words + i);
+                const uint64_t hi = (sh && i + 1 < a.dense_words) ? ld_u64(a.words + i + 1) : 0ull;
+                w0 = sh ? (lo << sh) | (hi >> (64 - sh)) : lo;
+            } else {
+                w0 = ld_u64(a.words + row * a.stride);
+            }
+            return (w0 & prefix_mask(min(m, kb))) >> (64 - 2 * kb);
+        };
+        const uint64_t kf = key_of(t0), kl = key_of(min(t0 + blockDim.x, a.Q) - 1);
+        const uint64_t xlo = k >= kb ? kf << (2 * (k - kb)) : kf >> (2 * (kb - k));
+        const uint64_t xhi = k >= kb ? (kl + 1) << (2 * (k - kb)) : (kl >> (2 * (kb - k))) + 1;
+        s_lo = min(max(ld_u32(a.table + xlo), a.clo), a.chi);
+        s_hi = min(max(ld_u32(a.table + xhi), a.clo), a.chi);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nodes * U4 * 16u)
+                     : "memory");
+    }
+    __syncthreads();
+    const uint32_t tlo = s_lo, thi = s_hi;
+    for (uint32_t i = threadIdx.x; i < nodes; i += blockDim.x) {
+        // the pivot of BFS node i+1: its path from the root, the same midpoints tree_descent takes
+        uint32_t Lp1 = tlo, R = thi;
+        const uint32_t node = i + 1;
+        for (int b = 30 - __clz(node); b >= 0; --b) {
+            const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
+            if ((node >> b) & 1) Lp1 = p + 1; else R = p;
+        }
+        uint64_t p = ((uint64_t)Lp1 - 1 + R) >> 1;
+        if (p < a.clo) p = a.clo;  // (an empty node's copy is never compared; keep its address valid)
+        if (p >= a.chi) p = a.chi - 1;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_nodes + (uint64_t)i * U4);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(a.rec + p * U4), "r"(U4 * 16u), "r"(bar) : "memory");
+    }
+    if (t < a.Q) {
+        uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
+        const uint64_t row = a.rows_ordered ? t : q;
+        const uint32_t m = read_len(a, row);
+        QueryWords<QW> P;
+        load_read<QW>(a, row, m, P);
+        uint32_t done = 0;  // the staged tree is complete (phase 0 of the barrier)
+        while (!done) {
+            asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0; selp.u32 %0, 1, 0, P1; }"
+                         : "=r"(done) : "r"(bar) : "memory");
+        }
+        const TreeCtx tc{s_nodes, tlo, thi, levels};
+        // (ubytes: the staged records are the CTA's, not counted per read)
+        uint32_t lo, hi, steps = 0, texts = 0, ubytes = ((m + 3) >> 2) + 8;
+        if (m >= k) search_read<L, true>(a, P, m, lo, hi, steps, texts, ubytes, &tc);
+        else search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
+        if (a.order) q = reload_u32(a.order + t);
+        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+        if (a.stats) {
+            a.stats[q] = min(steps, 0xFFFFu) | (min(texts, 0xFFFFu) << 16);
+            a.stats[a.Q + q] = ubytes;
+        }
+    } else {  // (every thread of the block waits before the block's shared memory can go away)
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0; selp.u32 %0, 1, 0, P1; }"
+                         : "=r"(done) : "r"(bar) : "memory");
+        }
     }
 }
 
@@ -714,11 +901,7 @@ __global__ void __launch_bounds__(256) k_match_group(const MatchArgs a) {
         P.init(a.words + row * a.stride, 0u, ~0ull, (m + 31) >> 5);
     }
     uint32_t lo, hi, steps = 0, texts = 0, ubytes = ((m + 3) >> 2) + 8;
-    if (m < a.min_len) {
-        lo = hi = 0xFFFFFFFFu;
-    } else {
-        search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
-    }
+    search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
     if (P.lane == 0) {
         reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
         if (STATS) {

@@ -123,44 +123,66 @@ def combine(summaries: List[List[int]]) -> List[int]:
 
 
 def partitioned_match(idx, words, lens=None, fixed_len=None, out=None):
-    """match this rank's batch against a partitioned index (idx = this rank's part).
+    """match this rank's batch against a partitioned index (idx = this rank's part,
+    csrc/sa_part.cu).
 
-    route (order by route key + rows in that order + per-destination offsets, sa_match_route) ->
-    all-to-all of the counts and of the rows -> match the received rows on this rank's slice ->
-    all-to-all of the intervals back -> sa_scatter_results into the batch's own order.  The
-    all-to-alls run over the default process group (NCCL on GPUs; gloo stages through host memory)."""
-    import paper_1303_3692_b200 as sa
+    route (order by route key, rows in that order, per-part offsets; reads shorter than the route key last:
+    sa_match_route) -> pack the send buffer (block g = the rows routed to part g + every short row:
+    sa_part_pack) -> all-to-all of the counts and of the rows -> match the received rows on this rank's
+    slice -> all-to-all of the intervals back -> sa_part_collect (a routed read takes its part's interval,
+    a short read the sum of the parts' clamped answers) into the batch's own order.  The all-to-alls run
+    over the default process group (NCCL on GPUs; gloo stages through host memory)."""
     Q, stride = words.shape
     dev = words.device
-    order, ow, ol, offs = idx.route(words, lens, fixed_len=fixed_len)
-    offs = offs.cpu().tolist()
-    send = [offs[g + 1] - offs[g] for g in range(len(offs) - 1)]
     world = dist.get_world_size() if dist.is_initialized() else 1
-    if world != len(send):
-        raise ValueError(f"{len(send)} partitions but world size {world}")
-    host = world > 1 and dist.get_backend() != "nccl"
-    stage = (lambda t: t.cpu()) if host else (lambda t: t)
-    if world == 1:
-        recv, rows, rlens = send, ow, ol
-    else:
-        st = torch.tensor(send, dtype=torch.int64, device="cpu" if host else dev)
-        rt = torch.empty_like(st)
-        dist.all_to_all_single(rt, st)
-        recv = rt.cpu().tolist()
-        rows = torch.empty((sum(recv), stride), dtype=words.dtype, device="cpu" if host else dev)
-        dist.all_to_all_single(rows, stage(ow), output_split_sizes=recv, input_split_sizes=send)
-        rows = rows.to(dev)
-        rlens = None
-        if ol is not None:
-            rlens = torch.empty(sum(recv), dtype=ol.dtype, device="cpu" if host else dev)
-            dist.all_to_all_single(rlens, stage(ol), output_split_sizes=recv, input_split_sizes=send)
-            rlens = rlens.to(dev)
+    order, ow, ol, offs = idx.route(words, lens, fixed_len=fixed_len)
+    o = offs.cpu().tolist()
+    nparts = len(o) - 1
+    if world != nparts:
+        raise ValueError(f"{nparts} partitions but world size {world}")
+    n_short = Q - o[nparts]
+    send = [o[g + 1] - o[g] + n_short for g in range(nparts)]
+    sw, sl = idx.part_pack(ow, ol, offs, sum(send))
+    recv, rows, rlens = exchange_rows(send, sw, sl, dev)
     res = idx.match(rows, rlens, fixed_len=fixed_len) if rows.shape[0] else \
         torch.empty((0, 2), dtype=torch.int32, device=dev)
+    back = exchange_back(res, recv, send, dev)
+    return idx.part_collect(back, offs, order, Q, out=out)
+
+
+def _host_staged():
+    return dist.is_initialized() and dist.get_world_size() > 1 and dist.get_backend() != "nccl"
+
+
+def exchange_rows(send, sw, sl, dev):
+    """All-to-all of the send blocks: (received counts per source, received rows, received lengths or None).
+    Rows from source s arrive in rank order: [block for me from rank 0, from rank 1, ...]."""
+    world = dist.get_world_size() if dist.is_initialized() else 1
     if world == 1:
-        back = res
-    else:
-        back = torch.empty((Q, 2), dtype=torch.int32, device="cpu" if host else dev)
-        dist.all_to_all_single(back, stage(res), output_split_sizes=send, input_split_sizes=recv)
-        back = back.to(dev)
-    return sa.scatter_results(order, back, out=out)
+        return list(send), sw, sl
+    host = _host_staged()
+    stage = (lambda t: t.cpu()) if host else (lambda t: t)
+    cdev = "cpu" if host else dev
+    st = torch.tensor(send, dtype=torch.int64, device=cdev)
+    rt = torch.empty_like(st)
+    dist.all_to_all_single(rt, st)
+    recv = rt.cpu().tolist()
+    rows = torch.empty((sum(recv),) + tuple(sw.shape[1:]), dtype=sw.dtype, device=cdev)
+    dist.all_to_all_single(rows, stage(sw), output_split_sizes=recv, input_split_sizes=list(send))
+    rlens = None
+    if sl is not None:
+        rlens = torch.empty(sum(recv), dtype=sl.dtype, device=cdev)
+        dist.all_to_all_single(rlens, stage(sl), output_split_sizes=recv, input_split_sizes=list(send))
+        rlens = rlens.to(dev)
+    return recv, rows.to(dev), rlens
+
+
+def exchange_back(res, recv, send, dev):
+    """All-to-all of the answers back to the ranks that sent the rows (the inverse split sizes)."""
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    if world == 1:
+        return res
+    host = _host_staged()
+    back = torch.empty((sum(send),) + tuple(res.shape[1:]), dtype=res.dtype, device="cpu" if host else dev)
+    dist.all_to_all_single(back, res.cpu() if host else res, output_split_sizes=list(send), input_split_sizes=recv)
+    return back.to(dev)

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libsynth.so")
 _lib = None
 
-REF_UNIFORM, REF_BACTERIAL, REF_REPEAT = 0, 1, 2
+REF_UNIFORM, REF_BACTERIAL, REF_REPEAT, REF_REPEAT_DUP = 0, 1, 2, 3
 
 
 def _load():
@@ -155,8 +155,8 @@ CONFIGS = {
                  "1 Mbp iid ACGT, 10k exact 32-bp reads + 10% random reads"),
     "C2": Config("C2", REF_BACTERIAL, 5_000_000, 2, 1_000_000, 25, 100, 0.0, 0.01, 2,
                  "5 Mbp E. coli-like, 1M reads of 25-100 bp, 1% of reads with one substitution"),
-    "C3": Config("C3", REF_REPEAT, 100_000_000, 3, 10_000_000, 100, 100, 0.10, 0.0, 3,
-                 "100 Mbp repeat-rich, 10M 100-bp reads (90% sampled, 10% random)"),
+    "C3": Config("C3", REF_REPEAT_DUP, 100_000_000, 3, 10_000_000, 100, 100, 0.10, 0.0, 3,
+                 "100 Mbp repeat-rich (+ one exact 100 kb duplication), 10M 100-bp reads (90% sampled, 10% random)"),
     "C4": Config("C4", REF_REPEAT, 3_100_000_000, 4, 100_000_000, 100, 100, 0.10, 0.0, 4,
                  "3.1 Gbp human-scale repeat-rich, 100M 100-bp reads (90% sampled, 10% random)"),
     "C5": Config("C5", REF_REPEAT, 3_100_000_000, 4, 50_000_000, 100, 100, 0.10, 0.0, 5100,

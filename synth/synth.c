@@ -73,7 +73,7 @@ static inline char substitute(rng_t *r, char c) {
 /* stream kinds */
 enum { K_BG = 1, K_PLAN, K_SEG, K_ALUFAM, K_L1FAM, K_SDFAM, K_READ, K_ELEM };
 
-enum { SYNTH_REF_UNIFORM = 0, SYNTH_REF_BACTERIAL = 1, SYNTH_REF_REPEAT = 2 };
+enum { SYNTH_REF_UNIFORM = 0, SYNTH_REF_BACTERIAL = 1, SYNTH_REF_REPEAT = 2, SYNTH_REF_REPEAT_DUP = 3 };
 
 static void set_threads(int nthreads) {
 #ifdef _OPENMP
@@ -283,7 +283,8 @@ static int gen_repeat(char *out, uint64_t n, uint64_t seed) {
 int synth_version(void) { return SYNTH_VERSION; }
 
 /* Writes n upper-case ACGT bytes to out.  kind: 0 uniform iid (C1), 1
- * E. coli-like (C2), 2 repeat-rich (C3/C4/C5).  Returns 0, or -1 on bad
+ * E. coli-like (C2), 2 repeat-rich (C4/C5), 3 repeat-rich + one exact 100 kb
+ * duplication (C3).  Returns 0, or -1 on bad
  * arguments / allocation failure. */
 int synth_reference(int kind, uint64_t n, uint64_t seed, char *out, int nthreads) {
     if (!out) return -1;
@@ -292,6 +293,15 @@ int synth_reference(int kind, uint64_t n, uint64_t seed, char *out, int nthreads
     case SYNTH_REF_UNIFORM: fill_background(out, n, seed, 0.5); return 0;
     case SYNTH_REF_BACTERIAL: gen_bacterial(out, n, seed); return 0;
     case SYNTH_REF_REPEAT: return gen_repeat(out, n, seed);
+    case SYNTH_REF_REPEAT_DUP: {
+        /* the repeat-rich recipe plus ONE exact (100 % identity) 100 kb segmental duplication: bases
+         * [n/4, n/4 + 100000) copied to [5n/8, 5n/8 + 100000) -- the deepest tie the suffix sort meets
+         * (segmental duplications at 99-100 % identity; reading B3) */
+        if (gen_repeat(out, n, seed) != 0) return -1;
+        const uint64_t L = 100000;
+        if (n >= 4 * L) memmove(out + 5 * (n / 8), out + n / 4, L);
+        return 0;
+    }
     default: return -1;
     }
 }

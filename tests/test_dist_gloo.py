@@ -82,3 +82,99 @@ def test_shard_ranges():
 def test_cpulist_parse():
     assert shard.parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
     assert shard.parse_cpulist("5") == [5]
+
+
+# ---- the partitioned index's exchange over a real 2-process group ---------------
+class FakePart:
+    """One part of a partitioned index computed on the CPU with the oracle, with the calls that
+    shard.partitioned_match makes (include/sa.h's contract for sa_match_route / sa_part_pack /
+    sa_match_batch on a part / sa_part_collect): the suffixes whose first rb bases (the route key, a short
+    suffix placed as the k-mer table places it) lie in [keys[g], keys[g+1]) form part g, whose ranks
+    [ranks[g], ranks[g+1]) tile [0, n); a part answers a read clamped to its ranks."""
+
+    def __init__(self, S, sa_ref, part, nparts, rb):
+        n = len(S)
+        T = oracle.kmer_table(S, rb).astype(np.int64)  # T_r[K] = #{i : trunc_rb(S_i) < K}
+        keys = [0] * (nparts + 1)
+        keys[nparts] = 4 ** rb
+        for g in range(1, nparts):
+            keys[g] = keys[g - 1] + int(np.searchsorted(T[keys[g - 1]:], g * n // nparts, side="left"))
+        self.S, self.sa, self.rb, self.P = S, sa_ref, rb, nparts
+        self.keys = keys
+        # (part 0 starts at rank 0: it also holds the all-'a' suffixes shorter than rb, e_rb = -1)
+        self.ranks = [0] + [int(T[keys[g]]) for g in range(1, nparts)] + [n]
+        self.r0, self.r1 = self.ranks[part], self.ranks[part + 1]
+
+    def route(self, words, lens=None, fixed_len=None):
+        w = words.numpy().view(np.uint64)
+        m = lens.numpy().astype(np.int64) if lens is not None else np.full(w.shape[0], fixed_len, np.int64)
+        rb = self.rb
+        key = (w[:, 0] >> np.uint64(64 - 2 * rb)).astype(np.int64)
+        short = m < rb
+        key[short] = 4 ** rb
+        order = np.argsort(key, kind="stable")
+        offs = np.searchsorted(key[order], self.keys, side="left").astype(np.int64)
+        ow = torch.from_numpy(w[order].view(np.int64).copy())
+        ol = None if lens is None else torch.from_numpy(lens.numpy()[order].copy())
+        return torch.from_numpy(order.astype(np.int32)), ow, ol, torch.from_numpy(offs)
+
+    def part_pack(self, ow, ol, offs, send_rows):
+        o = offs.tolist()
+        idx = np.concatenate([np.r_[o[g]:o[g + 1], o[self.P]:ow.shape[0]] for g in range(self.P)]).astype(np.int64)
+        assert idx.size == send_rows
+        return ow[idx], (None if ol is None else ol[idx])
+
+    def match(self, rows, rlens=None, fixed_len=None):
+        r = rows.numpy().view(np.uint64)
+        res = oracle.search_batch(self.S, self.sa, r, None if rlens is None else rlens.numpy().view(np.uint32),
+                                  fixed_len=fixed_len)
+        return torch.from_numpy(np.clip(res.astype(np.int64), self.r0, self.r1).astype(np.int32))
+
+    def part_collect(self, back, offs, order, Q, out=None):
+        o = offs.tolist()
+        b = back.numpy().astype(np.int64)
+        P, n_long = self.P, o[self.P]
+        n_short = Q - n_long
+        res = np.empty((Q, 2), np.int64)
+        for g in range(P):
+            B = o[g] + g * n_short
+            res[o[g]:o[g + 1]] = b[B:B + o[g + 1] - o[g]]
+        acc = np.zeros((n_short, 2), np.int64)
+        for g in range(P):
+            s0 = o[g + 1] + g * n_short
+            acc += b[s0:s0 + n_short] - self.ranks[g]
+        res[n_long:] = acc
+        out = np.empty_like(res)
+        out[order.numpy()] = res
+        return torch.from_numpy(out.astype(np.int32))
+
+
+def _part_worker(rank, world, port, outq):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ref = synth.reference(synth.REF_REPEAT, N_REF, 9)
+    S = oracle.encode(ref)
+    sa_ref = oracle.sa_naive(S)
+    part = FakePart(S, sa_ref, rank, world, 4)
+    # each rank its own batch, with reads shorter than the route key (sent to every part), and m = 0
+    words, lens = synth.reads(ref, 400 + 37 * rank, 0, 40, 0.1, 0.0, 20 + rank)
+    got = shard.partitioned_match(part, torch.from_numpy(words.view(np.int64)), torch.from_numpy(lens.view(np.int32)))
+    want = oracle.search_batch(S, sa_ref, words, lens).astype(np.int64)
+    outq.put((rank, bool(np.array_equal(got.numpy().astype(np.int64) & 0xFFFFFFFF, want)), int((lens < 4).sum())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_partitioned_exchange_two_ranks_gloo():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_part_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+    assert all(nshort > 0 for _, _, nshort in res)  # the multi-part (short read) path ran on both ranks

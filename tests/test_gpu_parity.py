@@ -297,6 +297,30 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     assert torch.equal(got2, base)
 
 
+@pytest.mark.parametrize("layout", ["rec16", "rec32"])
+@pytest.mark.parametrize("k", [0, 8, 12])
+@pytest.mark.parametrize("levels", [1, 5, 8, 12])
+def test_smem_tree_equals_oracle(layout, k, levels):
+    """SA_MATCH_SMEM_TREE (the per-CTA shared-memory top tree staged by TMA bulk copies) gives the oracle's
+    intervals: ordered reads of 10-128 bases (short reads take the plain path), a repeat-rich reference,
+    table k below / at / above the order's 12-base key."""
+    ref = synth.reference(synth.REF_REPEAT, 2_000_000, 55)
+    words, lens = synth.reads(ref, 100_000, 10, 128, 0.1, 0.02, 56)
+    rng = random.Random(levels)
+    hw, hl = synth.pack_strings(hazard_queries(ref.tobytes().decode(), 12, rng, extra=100), stride=4)
+    words, lens = np.concatenate([words, hw]), np.concatenate([lens, hl])
+    idx = sa.Index(ref, k=k, layout=layout)
+    S = oracle.encode(ref)
+    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
+    w = torch.from_numpy(words.view(np.int64)).cuda()
+    l = torch.from_numpy(lens.view(np.int32)).cuda()
+    for kb in (8, 12, 16):
+        perm = idx.order(w, l, key_bases=kb)
+        got = idx.match(w, l, order=perm, smem_tree=levels, tree_key_bases=kb).cpu().numpy().view(np.uint32)
+        bad = np.nonzero((got != want).any(axis=1))[0]
+        assert bad.size == 0, f"kb={kb}: {bad.size} mismatches, first {bad[0]}: {got[bad[0]]} vs {want[bad[0]]}"
+
+
 def _stable_key_order(words, lens, kb):
     key = (words[:, 0] >> np.uint64(64 - 2 * kb)).astype(np.uint64)
     m = lens.astype(np.uint64)

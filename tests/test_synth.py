@@ -67,3 +67,14 @@ def test_dense_layout_equals_packed_strings():
         d4, _ = synth.reads(ref, 96, m, m, 0.2, 0.0, 3, dense=True, nthreads=4)
         want = synth.pack_dense([synth.unpack_read(w[i], m) for i in range(96)])
         assert np.array_equal(d1, want[: d1.size]) and np.array_equal(d1, d4)
+
+
+def test_repeat_dup_has_one_exact_100kb_duplication():
+    # C3's recipe: the repeat-rich generator plus one exact 100 kb copy (reading B3)
+    n = 1_000_000
+    a = synth.reference(synth.REF_REPEAT, n, 3)
+    b = synth.reference(synth.REF_REPEAT_DUP, n, 3)
+    s, d, L = n // 4, 5 * (n // 8), 100_000
+    assert np.array_equal(b[d:d + L], b[s:s + L]) and np.array_equal(b[s:s + L], a[s:s + L])
+    assert np.array_equal(np.delete(b, np.s_[d:d + L]), np.delete(a, np.s_[d:d + L]))
+    assert synth.CONFIGS["C3"].ref_kind == synth.REF_REPEAT_DUP

@@ -28,10 +28,17 @@ def num(k):
     scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "Tbyte": 1e12}.get(u, 1)
     return x * scale
 dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+# the bench line of the profiled run names the exact configuration: traffic.json is keyed like
+# bench.py's traffic_key (workload/layout/k/reads per GPU) and holds DRAM bytes per read
+line = json.loads(open(os.path.join(root, "gpurun_out", f"prof_{tag}.json")).read().strip().splitlines()[-1])
+cfgj = line["config"]
+Q = cfgj["reads_per_gpu"]
+key = f"{workload}/{line['layout']}/k{cfgj['kmer_k']}/Q{Q}"
 tr_path = os.path.join(root, "profiles", "traffic.json")
 tr = json.load(open(tr_path)) if os.path.exists(tr_path) else {}
-tr[workload] = dram
-tr[f"_{workload}_source"] = f"profiles/{tag}_k_match_full_raw.csv (ncu --set full, one k_match launch)"
+tr = {k: v for k, v in tr.items() if isinstance(v, dict)}  # (drop the r01 flat entries)
+tr[key] = {"dram_bytes_per_read": dram / Q, "dram_bytes_per_launch": dram,
+           "source": f"profiles/{tag}_k_match_full_raw.csv (ncu --set full, one k_match launch of bench.py)"}
 json.dump(tr, open(tr_path, "w"), indent=1)
 # launch list shares
 txt = open(os.path.join(root, "gpurun_out", f"launches_{tag}.csv")).read()
@@ -42,7 +49,7 @@ for r in csv.DictReader(io.StringIO(txt)):
     a = agg.setdefault(name, [0, 0.0]); a[0] += 1; a[1] += float(r["Metric Value"])
 lines = [f"# {tag}: ncu summary ({workload})", "", "| metric | value |", "|---|---|"]
 lines += [f"| {k} | {v} {u} |" for k, (v, u) in m.items()]
-lines += ["", f"dram read+write per launch: {dram/1e9:.2f} GB", "", "Launch list (ncu gpu__time_duration.sum, serialised):", "",
+lines += ["", f"dram read+write per launch: {dram/1e9:.2f} GB = {dram/Q:.1f} B per read ({key})", "", "Launch list (ncu gpu__time_duration.sum, serialised):", "",
           "| kernel | launches | total ms |", "|---|---|---|"]
 lines += [f"| {k} | {c} | {t/1e6:.3f} |" for k, (c, t) in agg.items()]
 open(os.path.join(root, "profiles", f"{tag}_SUMMARY.md"), "w").write("\n".join(lines) + "\n")
