@@ -78,6 +78,8 @@ def parse():
                     help="the ordering step also gathers the read rows into order (SA_MATCH_ROWS_ORDERED)")
     ap.add_argument("--cooperative", action="store_true",
                     help="SA_MATCH_COOPERATIVE: reads over 128 bases searched by 8/16/32-lane groups")
+    ap.add_argument("--bucket-tree", action="store_true",
+                    help="SA_INDEX_BUCKET_TREE: line-packed binary-search trees for k-mer buckets of >= 32 suffixes")
     ap.add_argument("--smem-tree", type=int, default=0,
                     help="SA_MATCH_SMEM_TREE: levels (1..12) of the per-CTA shared-memory top tree staged by TMA "
                          "(SURVEY.md 8(a) a3(ii)); 0 = off")
@@ -372,7 +374,7 @@ def main():
     t0 = time.time()
     part = (rank, world, 12) if args.partition else None
     idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build, part=part,
-                   subtables=args.subtables)
+                   subtables=args.subtables, bucket_tree=args.bucket_tree)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     log(f"index built in {build_s:.1f}s: k={idx.k}, {idx.device_bytes / 1e9:.2f} GB resident")
@@ -497,7 +499,8 @@ def main():
             "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
                                           if presort else 0),
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
-            "shards": summary_all, "layout": args.layout, "smem_tree_levels": args.smem_tree, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
+            "shards": summary_all, "layout": args.layout, "smem_tree_levels": args.smem_tree,
+            "bucket_tree": args.bucket_tree, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
             "index_bytes": idx.device_bytes,
             "index_build": {"seconds": build_s, "sa_algorithm": args.build,
                             "note": "untimed: upload + pack + suffix array + k-mer table + records"}}

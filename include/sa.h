@@ -87,6 +87,11 @@ typedef struct {
  * bracket table over the next 4 bases (257 SA ranks each, found through a hash of the k-mer), so
  * reads of >= k+4 bases in such a bucket start from a bracket ~256x smaller. */
 #define SA_INDEX_SUBTABLE 8u
+/* sa_index_opts.flags (with SA_INDEX_REC32, not with SA_INDEX_SUBTABLE): every k-mer bucket of >= 32
+ * suffixes (repeats) also gets the records of the top levels of its binary search laid out two levels
+ * per 128-byte line (a pivot and both its children), found through a hash of the k-mer: a read in a
+ * large bucket makes the same probes, with about half as many DRAM lines.  Same results. */
+#define SA_INDEX_BUCKET_TREE 16u
 
 /* sa_match_batch flags. */
 #define SA_MATCH_STATS 1u  /* also write per-query search statistics into the workspace (the

@@ -30,6 +30,7 @@ SA_MATCH_COOPERATIVE = 32   # sa_match_batch flags: reads over 128 bases searche
 SA_MATCH_SMEM_TREE = 64     # sa_match_batch flags: shared-memory top tree per CTA (needs an order)
 SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 SA_INDEX_SUBTABLE = 8       # sa_index_opts.flags: (k+4)-base sub-tables for buckets of > 32 suffixes
+SA_INDEX_BUCKET_TREE = 16   # sa_index_opts.flags: line-packed binary-search trees for buckets of >= 32 suffixes
 LAYOUTS = {"rec16": 0, "rec32": SA_INDEX_REC32, "plain": SA_INDEX_PLAIN}
 _NAMES = {0: "SA_OK", -1: "SA_EINVAL", -2: "SA_ESYMBOL", -3: "SA_ETOOLONG", -4: "SA_ENOMEM", -5: "SA_ECUDA",
           -6: "SA_EEMPTY"}
@@ -149,14 +150,15 @@ class Index:
     """
 
     def __init__(self, ref, k: int = 0, device: Optional[int] = None, layout: str = "rec16", build: str = "doubling",
-                 part: Optional[Tuple[int, int, int]] = None, subtables: bool = False):
+                 part: Optional[Tuple[int, int, int]] = None, subtables: bool = False, bucket_tree: bool = False):
         if isinstance(ref, str):
             ref = ref.encode("ascii")
         arr = np.frombuffer(ref, dtype=np.uint8) if isinstance(ref, (bytes, bytearray)) else \
             np.ascontiguousarray(ref, dtype=np.uint8)
         if build not in ("doubling", "dc3"):
             raise ValueError("build must be 'doubling' or 'dc3'")
-        flags = LAYOUTS[layout] | (SA_INDEX_BUILD_DC3 if build == "dc3" else 0) | (SA_INDEX_SUBTABLE if subtables else 0)
+        flags = LAYOUTS[layout] | (SA_INDEX_BUILD_DC3 if build == "dc3" else 0) | (SA_INDEX_SUBTABLE if subtables else 0) | \
+            (SA_INDEX_BUCKET_TREE if bucket_tree else 0)
         opts = _Opts(-1 if device is None else int(device), int(k), flags, 0)
         self.layout = layout
         h = _p()

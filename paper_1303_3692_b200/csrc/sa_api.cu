@@ -32,6 +32,8 @@ void sa_free_index(sa_index *idx) {
     cudaFree(idx->big_hash);
     cudaFree(idx->big_sub);
     cudaFree(idx->route_table);
+    cudaFree(idx->tree);
+    cudaFree(idx->tree_hash);
     cudaFree(idx->part_ranks_dev);
     for (int b = 0; b < 2; ++b) {
         cudaFree(idx->pipe_words[b]);
@@ -59,9 +61,13 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     }
     sa_index_opts o{-1, 0, 0, 0};
     if (opts) o = *opts;
-    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32 | SA_INDEX_BUILD_DC3 | SA_INDEX_SUBTABLE)) != 0 ||
+    if ((o.flags & ~(SA_INDEX_PLAIN | SA_INDEX_REC32 | SA_INDEX_BUILD_DC3 | SA_INDEX_SUBTABLE | SA_INDEX_BUCKET_TREE)) != 0 ||
         (o.flags & (SA_INDEX_PLAIN | SA_INDEX_REC32)) == (SA_INDEX_PLAIN | SA_INDEX_REC32) || o.reserved != 0) {
         sa_set_error("unknown opts.flags bits / reserved must be 0");
+        return SA_EINVAL;
+    }
+    if ((o.flags & SA_INDEX_BUCKET_TREE) && (!(o.flags & SA_INDEX_REC32) || (o.flags & SA_INDEX_SUBTABLE))) {
+        sa_set_error("SA_INDEX_BUCKET_TREE needs SA_INDEX_REC32 and excludes SA_INDEX_SUBTABLE");
         return SA_EINVAL;
     }
     if (o.kmer_k > 16) { sa_set_error("kmer_k %u out of range 1..16", o.kmer_k); return SA_EINVAL; }
@@ -86,6 +92,7 @@ extern "C" sa_status sa_index_create(const char *ref_ascii, uint64_t n, const sa
     idx->layout = (o.flags & SA_INDEX_PLAIN) ? 0 : (o.flags & SA_INDEX_REC32) ? 2 : 1;
     idx->build_dc3 = (o.flags & SA_INDEX_BUILD_DC3) != 0;
     idx->subtables = (o.flags & SA_INDEX_SUBTABLE) != 0;
+    idx->bucket_tree = (o.flags & SA_INDEX_BUCKET_TREE) != 0;
     uint32_t k = o.kmer_k;
     if (k == 0) {  // auto: floor(log4 n) + 1 (mean bracket < 1 suffix), at most 16 (a 16 GiB table)
         k = 1;

@@ -185,6 +185,59 @@ __global__ void k_big_subtables(const uint64_t *__restrict__ text, uint64_t n, c
     }
 }
 
+// ---- bucket trees (SA_INDEX_BUCKET_TREE) ------------------------------------------------------------
+struct IsTreeBucket {
+    const uint32_t *T;
+    __host__ __device__ bool operator()(uint32_t x) const { return T[(uint64_t)x + 1] - T[x] >= kTreeMin; }
+};
+struct TreeLinesOf {  // lines of bucket x's tree: (4^E - 1) / 3
+    const uint32_t *T;
+    const uint32_t *xs;
+    __host__ __device__ uint64_t operator()(uint64_t id) const {
+        const uint32_t x = xs[id];
+        const uint32_t e = tree_pairs(T[(uint64_t)x + 1] - T[x]);
+        return ((1ull << (2 * e)) - 1) / 3;
+    }
+};
+
+__global__ void k_tree_hash_insert(const uint32_t *__restrict__ xs, const uint64_t *__restrict__ line0, uint64_t cnt,
+                                   uint32_t bits, unsigned long long *__restrict__ H) {
+    GRID_STRIDE(id, cnt) {
+        const uint32_t x = xs[id];
+        const uint64_t mask = (1ull << bits) - 1;
+        const unsigned long long e = ((unsigned long long)x << 32) | (uint32_t)line0[id];
+        for (uint64_t h = (uint64_t)((x * 0x9E3779B1u) >> (32 - bits));; h = (h + 1) & mask)
+            if (atomicCAS(&H[h], kBigEmpty, e) == kBigEmpty) break;
+    }
+}
+
+// one block per tree bucket: node i (BFS, 1-based) of the bucket's binary search over (T[x]-1, T[x+1])
+// at depth < 2E holds the record of its pivot -- the midpoints search_read takes -- at line
+// tree_line(pair root) slot 0 (pair root = a node at even depth), 1 (its left child) or 2 (its right)
+__global__ void k_tree_fill(const uint32_t *__restrict__ T, const uint32_t *__restrict__ xs, const uint64_t *__restrict__ line0,
+                            uint64_t cnt, const uint4 *__restrict__ rec, uint4 *__restrict__ tree) {
+    for (uint64_t id = blockIdx.x; id < cnt; id += gridDim.x) {
+        const uint32_t x = xs[id];
+        const uint32_t L0 = T[x], R0 = T[(uint64_t)x + 1];
+        const uint32_t E = tree_pairs(R0 - L0);
+        const uint32_t nodes = (1u << (2 * E)) - 1;
+        for (uint32_t i = 1 + threadIdx.x; i <= nodes; i += blockDim.x) {
+            uint32_t Lp1 = L0, R = R0;
+            for (int b = ilog2_u32(i) - 1; b >= 0; --b) {
+                const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
+                if ((i >> b) & 1) Lp1 = p + 1; else R = p;
+            }
+            uint64_t p = ((uint64_t)Lp1 - 1 + R) >> 1;
+            if (p < L0 || p >= R0) p = L0;  // an empty node: never probed
+            const uint32_t r = (ilog2_u32(i) & 1) ? (i >> 1) : i;
+            const uint32_t slot = i == r ? 0u : 1u + (i & 1u);
+            const uint64_t at = (line0[id] + tree_line(r)) * 4 + slot;  // in records of 32 bytes
+            tree[2 * at] = rec[2 * p];
+            tree[2 * at + 1] = rec[2 * p + 1];
+        }
+    }
+}
+
 template <typename F>
 sa_status cub_call(F f, cudaStream_t st, const char *what) {
     size_t bytes = 0;
@@ -373,6 +426,80 @@ sa_status sa_extract_sa(const sa_index *idx, uint32_t *host_out) {
     return SA_OK;
 }
 
+// the trees of every bucket of >= kTreeMin suffixes (after the records; k-mers in chunks of 2^30)
+sa_status build_bucket_trees(sa_index *idx, cudaStream_t st) {
+    const uint64_t K = 1ull << (2 * idx->k);
+    const uint64_t CH = 1ull << 30;
+    thrust::counting_iterator<uint32_t> xs(0);
+    DevBuf<int64_t> cnt;
+    SA_TRY(cnt.alloc(1, st, "tree bucket count"));
+    int64_t total = 0;
+    for (uint64_t x0 = 0; x0 < K; x0 += CH) {
+        const uint64_t len = (K - x0 < CH) ? K - x0 : CH;
+        thrust::transform_iterator<IsTreeBucket, thrust::counting_iterator<uint32_t>, int64_t> flag(xs + x0,
+                                                                                                 IsTreeBucket{idx->table});
+        SA_TRY(cub_call([&](void *tmp, size_t &bytes) {
+            return cub::DeviceReduce::Sum(tmp, bytes, flag, cnt.p, (int64_t)len, st);
+        }, st, "tree bucket count"));
+        int64_t c = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        total += c;
+    }
+    if (total == 0) return SA_OK;
+    DevBuf<uint32_t> big;
+    SA_TRY(big.alloc((uint64_t)total, st, "tree buckets"));
+    int64_t off = 0;
+    for (uint64_t x0 = 0; x0 < K; x0 += CH) {
+        const uint64_t len = (K - x0 < CH) ? K - x0 : CH;
+        SA_TRY(cub_call([&](void *tmp, size_t &bytes) {
+            return cub::DeviceSelect::If(tmp, bytes, xs + x0, big.p + off, cnt.p, (int64_t)len, IsTreeBucket{idx->table},
+                                         st);
+        }, st, "tree bucket select"));
+        int64_t c = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&c, cnt.p, 8, cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        off += c;
+    }
+    // first line of every bucket's tree: exclusive scan of its line counts
+    DevBuf<uint64_t> line0;
+    SA_TRY(line0.alloc((uint64_t)total + 1, st, "tree offsets"));
+    thrust::counting_iterator<uint64_t> ids(0);
+    thrust::transform_iterator<TreeLinesOf, thrust::counting_iterator<uint64_t>, uint64_t> lines(ids,
+                                                                                               TreeLinesOf{idx->table, big.p});
+    SA_TRY(cub_call([&](void *tmp, size_t &bytes) {
+        return cub::DeviceScan::ExclusiveSum(tmp, bytes, lines, line0.p, (int64_t)total, st);
+    }, st, "tree offsets scan"));
+    uint64_t last_off = 0, last_lines = 0;
+    SA_CUDA_TRY(cudaMemcpyAsync(&last_off, line0.p + total - 1, 8, cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    {
+        uint32_t x = 0, a = 0, b = 0;
+        SA_CUDA_TRY(cudaMemcpy(&x, big.p + total - 1, 4, cudaMemcpyDeviceToHost));
+        SA_CUDA_TRY(cudaMemcpy(&a, idx->table + x, 4, cudaMemcpyDeviceToHost));
+        SA_CUDA_TRY(cudaMemcpy(&b, idx->table + (uint64_t)x + 1, 4, cudaMemcpyDeviceToHost));
+        const uint32_t e = tree_pairs(b - a);
+        last_lines = ((1ull << (2 * e)) - 1) / 3;
+    }
+    const uint64_t nlines = last_off + last_lines;
+    if (nlines >= 0xFFFFFFFFull) { sa_set_error("bucket trees: too many lines"); return SA_ENOMEM; }
+    uint32_t bits = 1;
+    while ((1ull << bits) < 2ull * (uint64_t)total) ++bits;
+    SA_CUDA_TRY(cudaMalloc(&idx->tree, nlines * 128));
+    SA_CUDA_TRY(cudaMalloc(&idx->tree_hash, (1ull << bits) * sizeof(unsigned long long)));
+    SA_CUDA_TRY(cudaMemsetAsync(idx->tree_hash, 0xFF, (1ull << bits) * sizeof(unsigned long long), st));
+    k_tree_hash_insert<<<grid_for((uint64_t)total), kThreads, 0, st>>>(big.p, line0.p, (uint64_t)total, bits,
+                                                                       idx->tree_hash);
+    SA_CUDA_TRY(cudaGetLastError());
+    k_tree_fill<<<148 * 32, 128, 0, st>>>(idx->table, big.p, line0.p, (uint64_t)total, idx->rec, idx->tree);
+    SA_CUDA_TRY(cudaGetLastError());
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    idx->tree_count = (uint64_t)total;
+    idx->tree_lines = nlines;
+    idx->tree_bits = bits;
+    return SA_OK;
+}
+
 // idx->rec = the records of the `count` suffixes sa[0..count) (layout 1 or 2); trims the memory pool
 // first so the records can take the build's transient memory.
 sa_status sa_build_records(sa_index *idx, const uint32_t *sa, uint64_t count, cudaStream_t st) {
@@ -490,9 +617,12 @@ sa_status sa_build_index(sa_index *idx, const char *ref_ascii, cudaStream_t st) 
         idx->sa = nullptr;
         sa_bytes = n * (idx->layout == 2 ? 2 : 1) * sizeof(uint4);
     }
+    // ---- 5. bucket trees (SA_INDEX_BUCKET_TREE; rec32 records) ----
+    if (idx->bucket_tree && idx->layout == 2) SA_TRY(build_bucket_trees(idx, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     idx->device_bytes = idx->n_words * 8 + sa_bytes + (K + 1) * 4 + idx->big_count * 257 * 4 +
-                        (idx->big_count ? (1ull << idx->big_bits) * 8 : 0);
+                        (idx->big_count ? (1ull << idx->big_bits) * 8 : 0) + idx->tree_lines * 128 +
+                        (idx->tree_count ? (1ull << idx->tree_bits) * 8 : 0);
     // hand the build's transient memory back to the driver
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, idx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);

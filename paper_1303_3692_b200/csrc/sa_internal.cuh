@@ -73,6 +73,30 @@ struct DevBuf {
 // the index (immutable after create)
 constexpr uint32_t kBigBucket = 32;  // SA_INDEX_SUBTABLE threshold (suffixes per k-mer bucket)
 constexpr unsigned long long kBigEmpty = ~0ull;  // empty sub-table hash slot (no {x, id} entry equals it)
+constexpr uint32_t kTreeMin = 32;  // SA_INDEX_BUCKET_TREE: buckets of at least this many suffixes get a tree
+
+__host__ __device__ __forceinline__ int ilog2_u32(uint32_t v) {  // floor(log2 v), v > 0
+#ifdef __CUDA_ARCH__
+    return 31 - __clz(v);
+#else
+    return 31 - __builtin_clz(v);
+#endif
+}
+
+// SA_INDEX_BUCKET_TREE: the pair levels stored for a bucket of B suffixes -- depths 0 .. 2E-1 of its
+// binary search, E = max(1, (floor(log2 B) - 2) / 2): the deeper levels' intervals hold < ~8 suffixes,
+// whose records already share lines in the flat array
+__host__ __device__ __forceinline__ uint32_t tree_pairs(uint32_t B) {
+    const int lg = ilog2_u32(B | 1);
+    const int e = (lg - 2) / 2;
+    return e < 1 ? 1u : (uint32_t)e;
+}
+// line of pair root r (at depth 2e) in a bucket's tree: lines are numbered level by level (4^e per level)
+__host__ __device__ __forceinline__ uint64_t tree_line(uint32_t r) {
+    const int d = ilog2_u32(r);  // even
+    const uint64_t p4 = 1ull << d;        // 4^e
+    return (p4 - 1) / 3 + (r - p4);
+}
 constexpr uint64_t kGuardWords = 6;  // zero words past the text: windows up to base n + 159 are readable
 
 // SA values of the layout: base pointer + stride in uint32 units
@@ -99,6 +123,13 @@ struct sa_index {
     uint32_t big_bits = 0;       // log2 of the hash table size
     unsigned long long *big_hash = nullptr;  // dev: open addressing, x << 32 | sub-table id, empty = kBigEmpty
     uint32_t *big_sub = nullptr; // dev: big_count x 257 global SA ranks
+    // SA_INDEX_BUCKET_TREE: for every bucket of >= kTreeMin suffixes, the records of the top 2E levels of
+    // its binary search, 3 per 128-byte line (a pivot and its two children: two levels per DRAM line)
+    bool bucket_tree = false;
+    uint64_t tree_count = 0, tree_lines = 0;
+    uint32_t tree_bits = 0;
+    unsigned long long *tree_hash = nullptr;  // dev: x << 32 | first line of the bucket's tree, empty = ~0
+    uint4 *tree = nullptr;                    // dev: tree_lines x 128 bytes (4 record slots, 3 used)
     // partitioned index (sa_index_create_part, csrc/sa_part.cu): this index holds SA ranks
     // [rank_base, rank_end) and table entries [x_base, x_base + 4^(k-rb) * (keys in the part)] only:
     // the suffixes whose route key (first route_bases bases, sa_suffix_e) lies in

@@ -10,6 +10,7 @@
 #include "sa_internal.cuh"
 
 #include "sa_search.cuh"
+#include "sa_search_long.cuh"
 
 namespace {
 
@@ -19,6 +20,12 @@ template <int QW, int L, bool STATS>
 cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     const int threads = SA_MATCH_THREADS;
     const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+    if constexpr (L == sa_search::L_REC32) {
+        if (a.tree_hash) {  // SA_INDEX_BUCKET_TREE
+            sa_search::k_match<QW, L, STATS, true><<<blocks, threads, 0, st>>>(a);
+            return cudaGetLastError();
+        }
+    }
     sa_search::k_match<QW, L, STATS><<<blocks, threads, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -31,6 +38,24 @@ cudaError_t launch_g(const MatchArgs &a, cudaStream_t st) {
     if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidConfiguration;
     sa_search::k_match_group<G, WPL, L, STATS><<<(unsigned)blocks, threads, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+// long reads (more than 4 words): the warp-synchronous search with warp-cooperative text compares
+template <int L, bool STATS>
+cudaError_t launch_l(const MatchArgs &a, cudaStream_t st) {
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+    sa_search::k_match_long<L, STATS><<<blocks, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_long(const MatchArgs &a, int layout, bool stats, cudaStream_t st) {
+    using namespace sa_search;
+    switch (layout) {
+    case L_PLAIN: return stats ? launch_l<L_PLAIN, true>(a, st) : launch_l<L_PLAIN, false>(a, st);
+    case L_REC32: return stats ? launch_l<L_REC32, true>(a, st) : launch_l<L_REC32, false>(a, st);
+    default: return stats ? launch_l<L_REC16, true>(a, st) : launch_l<L_REC16, false>(a, st);
+    }
 }
 
 template <int QW>
@@ -358,6 +383,9 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.big_hash = idx->big_hash;
     a.big_sub = idx->big_sub;
     a.big_bits = idx->big_bits;
+    a.tree_hash = idx->tree_hash;
+    a.tree = idx->tree;
+    a.tree_bits = idx->tree_bits;
     a.clo = 0;
     a.chi = (uint32_t)idx->n;
     a.route = nullptr;
@@ -403,7 +431,12 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
     else if (nw <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
     else if (nw <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
+#ifndef SA_LONG_WARP  // one thread per read, two phases (k_match<0>); the A/B build SA_LONG_WARP takes
+                      // k_match_long (warp-synchronous rounds, warp-cooperative text compares)
     else if (!cooperative) e = launch_qw<0>(a, idx->layout, st_on, st);
+#else
+    else if (!cooperative) e = launch_long(a, idx->layout, st_on, st);
+#endif
     else if (nw <= 8) e = launch_group<8, 1>(a, idx->layout, st_on, st);
     else if (nw <= 16) e = launch_group<16, 1>(a, idx->layout, st_on, st);
     else if (nw <= 32) e = launch_group<32, 1>(a, idx->layout, st_on, st);

@@ -48,6 +48,9 @@ struct MatchArgs {
     const unsigned long long *__restrict__ big_hash; // SA_INDEX_SUBTABLE: x << 32 | sub-table id, empty = ~0
     const uint32_t *__restrict__ big_sub;
     uint32_t big_bits;
+    const unsigned long long *__restrict__ tree_hash;  // SA_INDEX_BUCKET_TREE: x << 32 | first line, empty = ~0
+    const uint4 *__restrict__ tree;                     // its lines (4 records of 32 bytes, 3 used)
+    uint32_t tree_bits;
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -578,11 +581,38 @@ __device__ __forceinline__ void compare_probe(const MatchArgs &a, const Probe<L>
     }
 }
 
+// SA_INDEX_BUCKET_TREE: a large bucket's binary search is an implicit tree (BFS node i: root 1, children
+// 2i, 2i+1 -- the probes of search_read and bound ARE its nodes); nodes above depth `depth` have their
+// records copied into lines of three (a node at even depth and its two children)
+struct TreeLoc {
+    uint64_t line0;  // the bucket's first line
+    uint32_t depth;  // levels stored (2E); 0 = no tree
+};
+
+__device__ __forceinline__ uint64_t tree_rec(const TreeLoc &tl, uint32_t i) {  // record index (32-byte units)
+    const uint32_t r = (ilog2_u32(i) & 1) ? (i >> 1) : i;
+    const uint32_t slot = i == r ? 0u : 1u + (i & 1u);
+    return (tl.line0 + tree_line(r)) * 4 + slot;
+}
+
+// the node's child after a probe (0: past the stored levels, or no tree)
+__device__ __forceinline__ uint32_t tree_child(const TreeLoc &tl, uint32_t node, bool left) {
+    if (!node) return 0;
+    const uint32_t c = 2 * node + (left ? 0u : 1u);
+    return c < (1u << tl.depth) ? c : 0u;
+}
+
 template <int L, class RD>
 __device__ __forceinline__ void probe(const MatchArgs &a, const RD &P, uint32_t m, uint64_t p,
-                                      uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts) {
+                                      uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts,
+                                      const TreeLoc &tl = TreeLoc{0, 0}, uint32_t node = 0) {
     Probe<L> pr;
-    pr.load(a, p);
+    if constexpr (L == L_REC32) {
+        if (node) pr.r.load(a.tree, tree_rec(tl, node));  // the same record, from the bucket's tree
+        else pr.load(a, p);
+    } else {
+        pr.load(a, p);
+    }
     compare_probe(a, pr, P, m, skip, in_bracket, sign, lcp, texts);
 }
 
@@ -598,16 +628,19 @@ __device__ __forceinline__ uint32_t probe_bytes(uint32_t m, uint32_t skip, uint3
 template <int L, class RD>
 __device__ __forceinline__ uint32_t bound(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1,
                                           uint32_t R, uint32_t lcpL, uint32_t lcpR, bool lower, bool in_bracket,
-                                          uint32_t &steps, uint32_t &texts, uint32_t &ubytes) {
+                                          uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
+                                          const TreeLoc &tl = TreeLoc{0, 0}, uint32_t node = 0) {
     while (R > Lp1) {
         const uint32_t p = (uint32_t)(((uint64_t)Lp1 - 1 + R) >> 1);
         int sign;
         uint32_t lcp;
         const uint32_t skip = min(lcpL, lcpR);
-        probe<L>(a, P, m, p, skip, in_bracket, sign, lcp, texts);
+        probe<L>(a, P, m, p, skip, in_bracket, sign, lcp, texts, tl, node);
         ++steps;
         ubytes += probe_bytes(m, skip, lcp);
-        if (sign < 0 || (lower && sign == 0)) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+        const bool left = sign < 0 || (lower && sign == 0);
+        if (left) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+        node = tree_child(tl, node, left);
     }
     return R;
 }
@@ -651,8 +684,15 @@ __device__ __forceinline__ bool tree_descent(const MatchArgs &a, const TreeCtx &
     return false;
 }
 
-// One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.
-template <int L, bool TREE = false, class RD>
+template <int L, bool TREE, class RD>
+__device__ __forceinline__ void joint_search(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1, uint32_t R,
+                                             uint32_t lcp0, const TreeLoc &tl, uint32_t node, uint32_t &lo,
+                                             uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
+                                             const TreeCtx *tc);
+
+// One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.  BT: the index may have
+// bucket trees (SA_INDEX_BUCKET_TREE; a separate instantiation keeps the default kernel's registers).
+template <int L, bool TREE = false, bool BT = false, class RD>
 __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uint32_t m, uint32_t &lo,
                                             uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
                                             const TreeCtx *tc = nullptr) {
@@ -701,8 +741,34 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
             }
         }
     }
-    uint32_t lcpL = 0, lcpR = 0;
-    uint32_t hLp1 = 0, hR = 0, hlcpL = 0, hlcpR = 0;
+    TreeLoc tl{0, 0};  // SA_INDEX_BUCKET_TREE: a large bucket's line-packed top levels
+    uint32_t node = 0;
+    if (BT && !TREE && a.tree_hash && R - Lp1 >= kTreeMin) {
+        const uint64_t mask = (1ull << a.tree_bits) - 1;
+        uint64_t h = (uint64_t)(((uint32_t)x * 0x9E3779B1u) >> (32 - a.tree_bits));
+        for (uint64_t tries = 0; tries <= mask; ++tries, h = (h + 1) & mask) {
+            const uint64_t e = ld_u64(reinterpret_cast<const uint64_t *>(a.tree_hash) + h);
+            if (e == ~0ull) break;
+            if ((uint32_t)(e >> 32) == (uint32_t)x) {
+                tl.line0 = (uint32_t)e;
+                tl.depth = 2 * tree_pairs(R - Lp1);
+                node = 1;
+                break;
+            }
+        }
+    }
+    joint_search<L, TREE>(a, P, m, Lp1, R, 0, tl, node, lo, hi, steps, texts, ubytes, tc);
+}
+
+// The joint lo/hi search over the bracket (Lp1 - 1, R) -- every suffix in it shares P's first lcp0
+// bases (lcp0 = 0: only the bracket property is known) -- with the split of search_read.
+template <int L, bool TREE, class RD>
+__device__ __forceinline__ void joint_search(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1, uint32_t R,
+                                             uint32_t lcp0, const TreeLoc &tl, uint32_t node, uint32_t &lo,
+                                             uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
+                                             const TreeCtx *tc) {
+    uint32_t lcpL = lcp0, lcpR = lcp0;
+    uint32_t hLp1 = 0, hR = 0, hlcpL = 0, hlcpR = 0, hnode = 0;
     bool split = false;
     if constexpr (TREE) split = tree_descent<L>(a, *tc, P, m, Lp1, R, lcpL, lcpR, hLp1, hR, hlcpL, hlcpR, steps, texts);
     while (!split && R > Lp1) {  // LB rule until the first pivot where P is a prefix of the suffix (the split)
@@ -710,16 +776,19 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
         int sign;
         uint32_t lcp;
         const uint32_t skip = min(lcpL, lcpR);
-        probe<L>(a, P, m, p, skip, true, sign, lcp, texts);
+        probe<L>(a, P, m, p, skip, true, sign, lcp, texts, tl, node);
         ++steps;
         ubytes += probe_bytes(m, skip, lcp);
         if (sign == 0) {  // lo lies in (L, p], hi in (p, R]: the RB search starts from here
             split = true;
             hLp1 = p + 1; hR = R; hlcpL = lcp; hlcpR = lcpR;
             R = p; lcpR = lcp;
+            hnode = tree_child(tl, node, false);
+            node = tree_child(tl, node, true);
             break;
         }
         if (sign < 0) { R = p; lcpR = lcp; } else { Lp1 = p + 1; lcpL = lcp; }
+        node = tree_child(tl, node, sign < 0);
     }
     if (!split) {  // no suffix has P as a prefix: an empty interval at the insertion point
         lo = hi = R;
@@ -727,8 +796,8 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
     }
     // finish the LB search in (L, p], then the RB search in (p, R at the split].  (Interleaving the
     // two chains, both probes issued before either compare, measured 3% slower at C4: profiles/r01n.)
-    lo = bound<L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts, ubytes);
-    hi = bound<L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts, ubytes);
+    lo = bound<L>(a, P, m, Lp1, R, lcpL, lcpR, true, true, steps, texts, ubytes, tl, node);
+    hi = bound<L>(a, P, m, hLp1, hR, hlcpL, hlcpR, false, true, steps, texts, ubytes, tl, hnode);
 }
 
 __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
@@ -763,7 +832,7 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 #define SA_MATCH_MINB_LONG (1024 / SA_MATCH_THREADS)
 #endif
 #define SA_MATCH_BOUNDS __launch_bounds__(SA_MATCH_THREADS, QW > 0 ? SA_MATCH_MINB : SA_MATCH_MINB_LONG)
-template <int QW, int L, bool STATS>
+template <int QW, int L, bool STATS, bool BT = false>
 __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.Q) return;
@@ -774,7 +843,25 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     load_read<QW>(a, row, m, P);
     // ubytes (SA_MATCH_STATS): the read (2 bits/base) + the 8-byte result + what the search adds
     uint32_t lo, hi, steps = 0, texts = 0, ubytes = ((m + 3) >> 2) + 8;
-    search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
+    if constexpr (QW == 0 && L != L_PLAIN) {
+        // Long reads in two phases.  (A) the search for P' = P's first mt = k + (cached bases) bases: the
+        // records decide every probe, no text is read.  Its interval holds P's: [lo, hi) within
+        // [lo', hi') (P' is a prefix of P).  (B) the joint search for P over [lo', hi'), where every
+        // suffix shares P' (compares start at base mt): for a unique hit one probe, the verification of
+        // P's remaining bases.  All lanes of a warp finish (A) before any starts (B), so the long
+        // text compares of (B) run with the warp's lanes together instead of one by one (ncu r02c: the
+        // one-phase kernel ran its text loop with 6 of 32 lanes active).
+        const uint32_t mt = min(m, a.k + Rec<L>::kBases);
+        search_read<L, false, BT>(a, P, mt, lo, hi, steps, texts, ubytes);
+        __syncwarp();
+        if (m > mt) {
+            if (hi > lo) joint_search<L, false>(a, P, m, lo, hi, mt, TreeLoc{0, 0}, 0, lo, hi, steps, texts, ubytes,
+                                                nullptr);
+            else hi = lo;
+        }
+    } else {
+        search_read<L, false, BT>(a, P, m, lo, hi, steps, texts, ubytes);
+    }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here.
     // The read index is loaded again here (an L1 hit) rather than kept live across the search: at the
     // 48 registers of the 62.5%-occupancy build ptxas otherwise spills it to local memory.

@@ -148,6 +148,29 @@ def test_subtables_k16_all_t_bucket(layout):
     check_full(text, qs, k=16, layout=layout, subtables=True)
 
 
+@pytest.mark.parametrize("k", [0, 6, 10, 14])
+def test_bucket_trees_equal_oracle(k):
+    """SA_INDEX_BUCKET_TREE (large buckets' binary-search pivots in line-packed trees) gives the oracle's
+    intervals: a repeat-rich reference + homopolymer / periodic runs (buckets of thousands of suffixes),
+    reads of 10-300 bases (short, record-decided and long two-phase kernels), the hazard batch."""
+    rng = random.Random(k)
+    ref = synth.reference(synth.REF_REPEAT, 1_500_000, 57).tobytes().decode()
+    ref += "A" * 3000 + "AC" * 2000 + "".join(rng.choice("ACGT") for _ in range(5000)) + "ACGTTGCA" * 700
+    words, lens = synth.reads(np.frombuffer(ref.encode(), dtype=np.uint8), 60_000, 10, 300, 0.1, 0.02, 58)
+    hw, hl = synth.pack_strings(hazard_queries(ref, k or 12, rng, extra=200) +
+                                ["A" * m for m in (12, 40, 100, 200, 300)] + ["AC" * 60, "ACGTTGCA" * 30],
+                                stride=words.shape[1])
+    words, lens = np.concatenate([words, hw]), np.concatenate([lens, hl])
+    idx, S, sa_ref, got = check_full(ref, words=words, lens=lens, k=k, layout="rec32", check_sa=False)
+    tree = sa.Index(ref, k=k, layout="rec32", bucket_tree=True)
+    assert tree.device_bytes > idx.device_bytes  # some buckets got trees
+    want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
+    for presort in (False, True):
+        g = gpu_match(tree, words, lens, presort=presort)
+        bad = np.nonzero((g != want).any(axis=1))[0]
+        assert bad.size == 0, f"{bad.size} mismatches, first {bad[0]} m={lens[bad[0]]}: {g[bad[0]]} vs {want[bad[0]]}"
+
+
 def test_subtables_repeat_rich():
     ref = synth.reference(synth.REF_REPEAT, 3_000_000, 35)
     words, lens = synth.reads(ref, 200_000, 16, 160, 0.1, 0.01, 36)

@@ -30,7 +30,7 @@ def num(k):
 dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
 # the bench line of the profiled run names the exact configuration: traffic.json is keyed like
 # bench.py's traffic_key (workload/layout/k/reads per GPU) and holds DRAM bytes per read
-line = json.loads(open(os.path.join(root, "gpurun_out", f"prof_{tag}.json")).read().strip().splitlines()[-1])
+line = json.loads([ln for ln in open(os.path.join(root, "gpurun_out", f"prof_{tag}.json")).read().splitlines() if ln.startswith("{")][-1])
 cfgj = line["config"]
 Q = cfgj["reads_per_gpu"]
 key = f"{workload}/{line['layout']}/k{cfgj['kmer_k']}/Q{Q}"
