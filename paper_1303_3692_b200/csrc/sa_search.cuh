@@ -262,6 +262,26 @@ __device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, 
 #ifdef SA_BULK_PREFETCH  // A/B build only: measured slower (r02b: m = 500 +18%, m = 1000 +7%)
         if (j0 >= 4) prefetch_rest(j0);
 #endif
+#ifdef SA_CHUNK2  // A/B build: two chunks (8 words, 256 bases) loaded per round trip
+        for (uint32_t c = j0 >> 2; 4 * c < nw; c += 2) {
+            uint64_t pa[4], pb[4] = {0, 0, 0, 0}, ta[4] = {0, 0, 0, 0}, tb[4] = {0, 0, 0, 0};
+            P.chunk(c, pa);
+            const bool two = 4 * (c + 1) < nw;
+            if (two) P.chunk(c + 1, pb);
+            if (128ull * c < slen) text_windows4(text, s + 128ull * c, ta);
+            if (two && 128ull * (c + 1) < slen) text_windows4(text, s + 128ull * (c + 1), tb);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * c + u;
+                if (j >= j0 && j < nw && cmp_word_window(slen, m, j, pa[u], ta[u], sign, lcp)) return;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * c + 4 + u;
+                if (j >= j0 && j < nw && cmp_word_window(slen, m, j, pb[u], tb[u], sign, lcp)) return;
+            }
+        }
+#else
         for (uint32_t c = j0 >> 2; 4 * c < nw; ++c) {
 #ifdef SA_BULK_PREFETCH
             if (4 * c > j0) prefetch_rest(4 * c);
@@ -275,6 +295,7 @@ __device__ __forceinline__ void compare_text(const uint64_t *__restrict__ text, 
                 if (j >= j0 && j < nw && cmp_word_window(slen, m, j, pw[u], tw[u], sign, lcp)) return;
             }
         }
+#endif
     }
     sign = 0;
     lcp = m;
