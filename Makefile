@@ -30,37 +30,42 @@ $(PKG)/libsa.so: $(CU_OBJS)
 
 $(shell mkdir -p build)
 
-# A/B build variants (variants/*.so; bench.py / tests load one with SA_LIB_PATH=...)
-VARIANTS := variants/libsa_ldcg.so variants/libsa_ldnoalloc.so variants/libsa_ldca.so variants/libsa_l2_64.so \
-            variants/libsa_l2_64na.so variants/libsa_t128.so variants/libsa_t64.so variants/libsa_t128_m12.so \
-            variants/libsa_t64_m32.so variants/libsa_t256_m6.so variants/libsa_t64_m24.so variants/libsa_t128_m10.so \
-            variants/libsa_t64_m20.so variants/libsa_t256_m1.so variants/libsa_outpad.so variants/libsa_t256_m5.so \
-            variants/libsa_head1.so variants/libsa_head2.so variants/libsa_head3.so variants/libsa_head1_m5.so \
-            variants/libsa_bulkpf.so
-variants/libsa_ldcg.so: DEFS := -DSA_LD_MODE=1
-variants/libsa_ldnoalloc.so: DEFS := -DSA_LD_MODE=2
-variants/libsa_ldca.so: DEFS := -DSA_LD_MODE=3
-variants/libsa_l2_64.so: DEFS := -DSA_LD_MODE=4
-variants/libsa_l2_64na.so: DEFS := -DSA_LD_MODE=5
-variants/libsa_t128.so: DEFS := -DSA_MATCH_THREADS=128
-variants/libsa_t64.so: DEFS := -DSA_MATCH_THREADS=64
-variants/libsa_t128_m12.so: DEFS := -DSA_MATCH_THREADS=128 -DSA_MATCH_MINB=12
-variants/libsa_t64_m32.so: DEFS := -DSA_MATCH_THREADS=64 -DSA_MATCH_MINB=32
-variants/libsa_t64_m24.so: DEFS := -DSA_MATCH_THREADS=64 -DSA_MATCH_MINB=24
-variants/libsa_t256_m6.so: DEFS := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=6
-variants/libsa_t128_m10.so: DEFS := -DSA_MATCH_THREADS=128 -DSA_MATCH_MINB=10
-variants/libsa_t64_m20.so: DEFS := -DSA_MATCH_THREADS=64 -DSA_MATCH_MINB=20
-variants/libsa_t256_m1.so: DEFS := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=1
-variants/libsa_outpad.so: DEFS := -DSA_OUT_PAD=1
-variants/libsa_t256_m5.so: DEFS := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=5
-variants/libsa_head1.so: DEFS := -DSA_QW0_HEAD=1
-variants/libsa_head2.so: DEFS := -DSA_QW0_HEAD=2
-variants/libsa_head3.so: DEFS := -DSA_QW0_HEAD=3
-variants/libsa_head1_m5.so: DEFS := -DSA_QW0_HEAD=1 -DSA_MATCH_MINB=5
-variants/libsa_bulkpf.so: DEFS := -DSA_BULK_PREFETCH
-variants: $(VARIANTS)
-variants/%.so: $(CU_SRCS) $(CU_HDRS)
-	mkdir -p variants && $(NVCC) $(NVFLAGS) $(DEFS) -Iinclude -shared -o $@ $(CU_SRCS) -lcudart 2> build/ptxas_$(notdir $@).log || (cat build/ptxas_$(notdir $@).log; false)
+# A/B build variants (variants/*.so; bench.py / tests / tools/ab_libs.py load one with SA_LIB_PATH=... or
+# --libs): sa_match.cu (the search kernels) recompiled with the defines, linked with the default objects
+VARIANTS := ldcg ldnoalloc ldca l2_64 l2_64na t128 t64 t128_m12 t64_m32 t256_m6 t64_m24 t128_m10 t64_m20 \
+            t256_m1 outpad t256_m5 head1 head2 head3 head1_m5 bulkpf chunk2m3 m3 longwarp dual dual3 hostnoorder \
+            packed
+DEFS_ldcg := -DSA_LD_MODE=1
+DEFS_ldnoalloc := -DSA_LD_MODE=2
+DEFS_ldca := -DSA_LD_MODE=3
+DEFS_l2_64 := -DSA_LD_MODE=4
+DEFS_l2_64na := -DSA_LD_MODE=5
+DEFS_t128 := -DSA_MATCH_THREADS=128
+DEFS_t64 := -DSA_MATCH_THREADS=64
+DEFS_t128_m12 := -DSA_MATCH_THREADS=128 -DSA_MATCH_MINB=12
+DEFS_t64_m32 := -DSA_MATCH_THREADS=64 -DSA_MATCH_MINB=32
+DEFS_t64_m24 := -DSA_MATCH_THREADS=64 -DSA_MATCH_MINB=24
+DEFS_t256_m6 := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=6
+DEFS_t128_m10 := -DSA_MATCH_THREADS=128 -DSA_MATCH_MINB=10
+DEFS_t64_m20 := -DSA_MATCH_THREADS=64 -DSA_MATCH_MINB=20
+DEFS_t256_m1 := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=1
+DEFS_outpad := -DSA_OUT_PAD=1
+DEFS_t256_m5 := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=5
+DEFS_head1 := -DSA_QW0_HEAD=1
+DEFS_head2 := -DSA_QW0_HEAD=2
+DEFS_head3 := -DSA_QW0_HEAD=3
+DEFS_head1_m5 := -DSA_QW0_HEAD=1 -DSA_MATCH_MINB=5
+DEFS_bulkpf := -DSA_BULK_PREFETCH
+DEFS_chunk2m3 := -DSA_CHUNK2 -DSA_MATCH_MINB_LONG=3
+DEFS_m3 := -DSA_MATCH_MINB_LONG=3
+DEFS_longwarp := -DSA_LONG_WARP
+DEFS_dual := -DSA_MATCH_DUAL
+DEFS_dual3 := -DSA_MATCH_DUAL -DSA_DUAL_MINB=3
+DEFS_hostnoorder := -DSA_HOST_NO_ORDER
+DEFS_packed := -DSA_ORDER_PACKED
+variants: $(addprefix variants/libsa_,$(addsuffix .so,$(VARIANTS)))
+variants/libsa_%.so: $(CU_OBJS) $(CU_HDRS)
+	bash tools/variant.sh $* "$(DEFS_$*)"
 
 clean:
 	rm -f synth/libsynth.so oracle/liboracle.so $(PKG)/libsa.so

@@ -83,8 +83,11 @@ def parse():
     ap.add_argument("--smem-tree", type=int, default=0,
                     help="SA_MATCH_SMEM_TREE: levels (1..12) of the per-CTA shared-memory top tree staged by TMA "
                          "(SURVEY.md 8(a) a3(ii)); 0 = off")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the step's ordering and match launches in two CUDA graphs, replayed each step")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=0, help="reads per chunk of the host pipeline (0 = library default)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-locate", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -457,6 +460,33 @@ def main():
         step()
     torch.cuda.synchronize()
 
+    graphs = None
+    if args.graph and presort and chunks == 1 and not (args.partition or tree is not None or rows_ordered):
+        # the step's launches (key extraction, CUB's sort kernels, k_match) captured once and replayed:
+        # no per-launch CPU work or inter-kernel launch gaps inside a step
+        g_order, g_match = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(device=dev)
+        cs.wait_stream(stream)
+        with torch.cuda.graph(g_order, stream=cs):
+            idx.order(words, lens, fixed_len=fixed, out=perm, stream=cs, workspace=ws, key_bases=args.order_bases)
+        with torch.cuda.graph(g_match, stream=cs):
+            idx.match(words, lens, fixed_len=fixed, out=out, stream=cs, workspace=ws, order=perm,
+                      smem_tree=args.smem_tree, tree_key_bases=args.order_bases)
+        stream.wait_stream(cs)
+        graphs = (g_order, g_match)
+
+        def step(i=None):  # noqa: F811  (the same step, replayed from the graphs)
+            g_order.replay()
+            if i is not None:
+                ev[i][0].record(stream)
+            g_match.replay()
+            if i is not None:
+                ev[i][1].record(stream)
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+
     # ---- timed region ----
     if world > 1:
         dist.barrier()
@@ -500,7 +530,7 @@ def main():
                                           if presort else 0),
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
             "shards": summary_all, "layout": args.layout, "smem_tree_levels": args.smem_tree,
-            "bucket_tree": args.bucket_tree, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
+            "bucket_tree": args.bucket_tree, "cuda_graphs": graphs is not None, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",
             "index_bytes": idx.device_bytes,
             "index_build": {"seconds": build_s, "sa_algorithm": args.build,
                             "note": "untimed: upload + pack + suffix array + k-mer table + records"}}
@@ -645,6 +675,7 @@ def main():
         out_h = torch.empty((Q, 2), dtype=torch.int32, pin_memory=True)
         on = out_h.numpy()
         kw = {"n_reads": Q} if dense else {}
+        kw["chunk"] = args.e2e_chunk
         idx.match_host(wn, ln, fixed_len=fixed, out=on, **kw)  # warm-up (allocates staging)
         e2e_steps = max(1, min(args.steps, 5))
         if world > 1:
@@ -659,7 +690,8 @@ def main():
         line["e2e"] = {"value": global_reads * e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": Q * 8, "steps": e2e_steps,
                        "layout": "dense 2-bit stream" if dense else f"{stride} words per read",
-                       "path": "sa_match_batch_host (pinned host buffers, 2 streams, 4M-read chunks, each ordered)",
+                       "path": "sa_match_batch_host (pinned host buffers, 2 streams, "
+                               f"{args.e2e_chunk or 4 << 20}-read chunks, each ordered)",
                        "overlapped_ms_per_step": dt * 1e3 / e2e_steps}
         # the paper's Table V split (input / kernel / output time), measured one phase at a
         # time without overlap: H2D of the reads, ordering + search on the device copy, D2H of the intervals

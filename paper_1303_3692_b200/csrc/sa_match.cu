@@ -11,6 +11,7 @@
 
 #include "sa_search.cuh"
 #include "sa_search_long.cuh"
+#include "sa_search_dual.cuh"
 
 namespace {
 
@@ -20,6 +21,15 @@ template <int QW, int L, bool STATS>
 cudaError_t launch_t(const MatchArgs &a, cudaStream_t st) {
     const int threads = SA_MATCH_THREADS;
     const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+#ifdef SA_MATCH_DUAL  // A/B build: two reads per thread (sa_search_dual.cuh)
+    if constexpr (QW > 0 && !STATS) {
+        if (!a.tree_hash && !a.big_sub) {
+            const uint64_t half = (a.Q + 1) / 2;
+            sa_search::k_match_dual<QW, L><<<(unsigned)((half + 255) / 256), 256, 0, st>>>(a, half);
+            return cudaGetLastError();
+        }
+    }
+#endif
     if constexpr (L == sa_search::L_REC32) {
         if (a.tree_hash) {  // SA_INDEX_BUCKET_TREE
             sa_search::k_match<QW, L, STATS, true><<<blocks, threads, 0, st>>>(a);
@@ -101,7 +111,7 @@ cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t s
 __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens,
                                uint32_t fixed_len, uint32_t stride, uint64_t dense_words, uint64_t Q,
                                uint32_t key_bases, bool short_last, uint32_t *__restrict__ keys,
-                               uint32_t *__restrict__ perm) {
+                               uint32_t *__restrict__ perm, uint64_t *__restrict__ k64) {
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t m;
         uint64_t w0;
@@ -117,8 +127,13 @@ __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_
             w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
         }
         const uint32_t pre = (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases));
-        keys[q] = (short_last && m < key_bases) ? (1u << (2 * key_bases)) : pre;
-        perm[q] = (uint32_t)q;
+        const uint32_t key = (short_last && m < key_bases) ? (1u << (2 * key_bases)) : pre;
+        if (k64) {  // (SA_ORDER_PACKED)
+            k64[q] = ((uint64_t)key << 27) | q;
+        } else {
+            keys[q] = key;
+            perm[q] = (uint32_t)q;
+        }
     }
 }
 
@@ -153,13 +168,24 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
     if (stats) { L.stats = off; off = align256(off + Q * 8); }
     if (presort) {
         if (Q >= (1ull << 32)) { sa_set_error("read ordering needs Q < 2^32"); return SA_EINVAL; }
+#ifdef SA_ORDER_PACKED  // A/B build: (key << 27 | read) sorted as one 64-bit key (keys_in/keys_out hold 8 B each)
+        L.keys_in = off; off = align256(off + Q * 8);
+        L.keys_out = off; off = align256(off + Q * 8);
+        L.perm_in = off; off = align256(off + Q * 4);
+#else
         L.keys_in = off; off = align256(off + Q * 4);
         L.keys_out = off; off = align256(off + Q * 4);
         L.perm_in = off; off = align256(off + Q * 4);
+#endif
         if (!order_only) { L.perm_out = off; off = align256(off + Q * 4); }
         size_t b = 0;
+#ifdef SA_ORDER_PACKED
+        cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, b, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                                       (int64_t)Q, 27, 64);
+#else
         cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                                         (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)Q, 0, 32);
+#endif
         if (e != cudaSuccess) { sa_set_error("order size query: %s", cudaGetErrorString(e)); return SA_ECUDA; }
         L.cub = off;
         L.cub_bytes = b;
@@ -171,6 +197,14 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
 
 constexpr uint32_t kDefaultKeyBases = 12;
 
+#ifdef SA_ORDER_PACKED
+// the sorted packed keys (key << 27 | read index) -> the permutation
+__global__ void k_unpack_order(const uint64_t *__restrict__ k64, uint64_t Q, uint32_t *__restrict__ order) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (uint64_t)gridDim.x * blockDim.x)
+        order[t] = (uint32_t)(k64[t] & ((1u << 27) - 1));
+}
+#endif
+
 sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len, uint32_t stride, uint64_t Q,
                       uint32_t key_bases, uint8_t *ws, const PresortLayout &L, uint32_t *order, cudaStream_t st,
                       bool short_last = false) {
@@ -180,9 +214,6 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     uint64_t blocks = (Q + 255) / 256;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     const uint64_t dense_words = (Q * (uint64_t)fixed_len + 31) / 32;
-    k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
-                                                     short_last, keys_in, perm_in);
-    SA_CUDA_TRY(cudaGetLastError());
     size_t b = L.cub_bytes;
     // key = the first key_bases bases: ceil(2*key_bases/8) radix passes.  Measured and dropped
     // (profiles/r01-3): 32-bit offsets (CUB's 23-items-per-thread tuning) +0.5 ms per 100 M reads; a
@@ -190,6 +221,23 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     // 4-byte stores are partial-sector DRAM read-modify-writes: 5.6 GB written, 5.2 GB read per pass
     // for 0.8 GB of payload; CUB's 8-bit digits keep each bin's run long enough to coalesce).
     const int end_bit = 2 * (int)key_bases + (short_last ? 1 : 0);
+#ifdef SA_ORDER_PACKED
+    if (!short_last && Q < (1ull << 27)) {
+        // keys_in .. perm_in hold the packed 64-bit keys; keys_out .. (+8 B) the sorted ones
+        uint64_t *k64 = reinterpret_cast<uint64_t *>(ws + L.keys_in);
+        uint64_t *k64o = reinterpret_cast<uint64_t *>(ws + L.keys_out);
+        k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
+                                                         short_last, nullptr, nullptr, k64);
+        SA_CUDA_TRY(cudaGetLastError());
+        SA_CUDA_TRY(cub::DeviceRadixSort::SortKeys(ws + L.cub, b, k64, k64o, (int64_t)Q, 27, 27 + end_bit, st));
+        k_unpack_order<<<(unsigned)blocks, 256, 0, st>>>(k64o, Q, order);
+        SA_CUDA_TRY(cudaGetLastError());
+        return SA_OK;
+    }
+#endif
+    k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
+                                                     short_last, keys_in, perm_in, nullptr);
+    SA_CUDA_TRY(cudaGetLastError());
     SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0,
                                                 end_bit, st));
     return SA_OK;

@@ -52,5 +52,22 @@ lines += [f"| {k} | {v} {u} |" for k, (v, u) in m.items()]
 lines += ["", f"dram read+write per launch: {dram/1e9:.2f} GB = {dram/Q:.1f} B per read ({key})", "", "Launch list (ncu gpu__time_duration.sum, serialised):", "",
           "| kernel | launches | total ms |", "|---|---|---|"]
 lines += [f"| {k} | {c} | {t/1e6:.3f} |" for k, (c, t) in agg.items()]
+# the bench steps only (from the first read-ordering launch on): each kernel's share of a step
+rows = list(csv.DictReader(io.StringIO(txt)))
+first = next((i for i, r in enumerate(rows) if "k_presort_keys" in r["Kernel Name"]), None)
+if first is not None:
+    step = collections.OrderedDict()
+    import re
+    for r in rows[first:]:
+        name = r["Kernel Name"].split("(")[0].replace("<unnamed>::", "")[:80]
+        if re.search(r"k_match\w*<[^>]*?, 1[,>]", name) and re.search(r"k_match<\d+, \d+, 1", name):
+            break  # the instrumented (SA_MATCH_STATS) launch after the timed steps
+        if not any(x in name for x in ("k_presort_keys", "DeviceRadixSort", "k_match")):
+            continue
+        a = step.setdefault(name, [0, 0.0]); a[0] += 1; a[1] += float(r["Metric Value"])
+    tot = sum(t for _, t in step.values())
+    lines += ["", "Timed steps only (ordering + match launches of bench.py's steps; ncu, serialised, cold caches):", "",
+              "| kernel | launches | total ms | share |", "|---|---|---|---|"]
+    lines += [f"| {k} | {c} | {t/1e6:.3f} | {t/tot:.3f} |" for k, (c, t) in step.items()]
 open(os.path.join(root, "profiles", f"{tag}_SUMMARY.md"), "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
