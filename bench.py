@@ -83,8 +83,8 @@ def parse():
     ap.add_argument("--smem-tree", type=int, default=0,
                     help="SA_MATCH_SMEM_TREE: levels (1..12) of the per-CTA shared-memory top tree staged by TMA "
                          "(SURVEY.md 8(a) a3(ii)); 0 = off")
-    ap.add_argument("--graph", action="store_true",
-                    help="capture the step's ordering and match launches in two CUDA graphs, replayed each step")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the step's kernels one by one instead of replaying them from two CUDA graphs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=0, help="reads per chunk of the host pipeline (0 = library default)")
@@ -375,7 +375,12 @@ def main():
     ref = cfg.reference()
     log(f"{cfg.name}: reference of {cfg.n} bases generated in {time.time() - t0:.1f}s")
     t0 = time.time()
-    part = (rank, world, 12) if args.partition else None
+    k_auto = args.k
+    if not k_auto:  # the library's auto k: floor(log4 n) + 1, at most 16
+        k_auto = 1
+        while k_auto < 16 and 4 ** k_auto <= cfg.n:
+            k_auto += 1
+    part = (rank, world, min(12, k_auto - 1)) if args.partition else None  # route key: < k, <= 12 bases
     idx = sa.Index(ref, k=args.k, device=local, layout=args.layout, build=args.build, part=part,
                    subtables=args.subtables, bucket_tree=args.bucket_tree)
     torch.cuda.synchronize()
@@ -461,7 +466,8 @@ def main():
     torch.cuda.synchronize()
 
     graphs = None
-    if args.graph and presort and chunks == 1 and not (args.partition or tree is not None or rows_ordered):
+    if args.graph and presort and chunks == 1 and not (args.partition or tree is not None or rows_ordered or
+                                                       args.smem_tree or args.cooperative):
         # the step's launches (key extraction, CUB's sort kernels, k_match) captured once and replayed:
         # no per-launch CPU work or inter-kernel launch gaps inside a step
         g_order, g_match = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -691,7 +697,7 @@ def main():
                        "d2h_bytes_per_step": Q * 8, "steps": e2e_steps,
                        "layout": "dense 2-bit stream" if dense else f"{stride} words per read",
                        "path": "sa_match_batch_host (pinned host buffers, 2 streams, "
-                               f"{args.e2e_chunk or 4 << 20}-read chunks, each ordered)",
+                               f"{args.e2e_chunk or 2 << 20}-read chunks, each ordered)",
                        "overlapped_ms_per_step": dt * 1e3 / e2e_steps}
         # the paper's Table V split (input / kernel / output time), measured one phase at a
         # time without overlap: H2D of the reads, ordering + search on the device copy, D2H of the intervals

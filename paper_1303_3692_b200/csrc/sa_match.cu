@@ -549,7 +549,7 @@ extern "C" sa_status sa_match_batch_host(sa_index *idx, const uint64_t *q_words,
     if (Q == 0) return SA_OK;
     std::lock_guard<std::mutex> lock(idx->mu);
     SA_CUDA_TRY(cudaSetDevice(idx->device));
-    if (chunk_Q == 0) chunk_Q = 1ull << 22;
+    if (chunk_Q == 0) chunk_Q = 1ull << 21;  // 2 M reads: the best of 1 / 2 / 4 / 8 / 16 M (profiles/r02/r02j)
     chunk_Q = (chunk_Q + 31) & ~31ull;  // dense layout: every chunk starts on a word boundary
     if (chunk_Q > Q) chunk_Q = Q;
     // words of `cq` reads starting at read q0 (q0 a multiple of chunk_Q, hence of 32 for dense)

@@ -78,3 +78,19 @@ def test_gpus_without_matching_world_size_fails():
                        capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+@pytest.mark.gpu
+def test_partitioned_two_ranks_equal_replicated():
+    """SURVEY.md 8(f) f4 end to end: `--partition` with 2 self-launched ranks (gloo, one GPU) exchanges the
+    reads with real all-to-alls; the per-shard summaries (hits, sum of counts, checksum of every interval)
+    equal those of the replicated index on the same reads."""
+    import sys as _sys
+    _sys.path.insert(0, ROOT)
+    from paper_1303_3692_b200 import shard
+    args = ["--gpus", "2", "--dist-backend", "gloo", "--config", "C2", "--steps", "3", "--warmup", "3", "--no-cpu",
+            "--no-e2e", "--no-locate"]
+    rep = _run(args, 900, env=_clean_env())
+    part = _run(args + ["--partition"], 900, env=_clean_env())
+    assert part["n_gpus"] == 2 and part["partition"]["nparts"] == 2
+    assert shard.combine(part["shards"]) == shard.combine(rep["shards"])
