@@ -510,3 +510,28 @@ def test_c4_full_size():
 def test_c5_read_lengths_full_reference(m):
     # C5's reference (= C4's) at a sample of its read lengths; 2M reads per length
     _full_size_check(synth.CONFIGS["C5"].with_m(m), sample=128, q_count=2_000_000)
+
+
+def test_k16_table_sampled_against_oracle():
+    """The bench's k = 16 table (4^16 + 1 entries, 17 GB -- too large for the oracle's histogram table): T[x]
+    = #{i : trunc_16(S_i) < x} = lo(x) for the 16-mer x, so sampled entries are checked against the oracle's
+    textbook search of x (k-mers of the text, their neighbours, random, the first and last), plus T's
+    monotonicity and T[4^16] = n over the whole exported table."""
+    ref = synth.reference(synth.REF_REPEAT, 1_000_000, 81)
+    idx = sa.Index(ref, k=16, layout="rec32")
+    T = idx.export_table()
+    assert T.size == (1 << 32) + 1 and T[-1] == len(ref) and T[0] == 0
+    assert np.all(T[1:] >= T[:-1])
+    S = oracle.encode(ref)
+    sa_ref = oracle.sa_naive(S)
+    rng = np.random.default_rng(82)
+    pos = rng.integers(0, len(ref) - 16, 3000)
+    codes = np.zeros(pos.size, dtype=np.uint64)
+    for j in range(16):
+        codes = (codes << np.uint64(2)) | S[pos + j].astype(np.uint64)
+    xs = np.concatenate([codes, codes + np.uint64(1), codes - np.uint64(1),
+                         rng.integers(0, 1 << 32, 2000, dtype=np.uint64),
+                         np.array([0, 1, (1 << 32) - 1], dtype=np.uint64)]) & np.uint64((1 << 32) - 1)
+    words = (xs << np.uint64(32)).reshape(-1, 1)
+    want = oracle.search_batch(S, sa_ref, words, None, fixed_len=16)[:, 0]
+    assert np.array_equal(T[xs.astype(np.int64)].astype(np.uint64), want)
