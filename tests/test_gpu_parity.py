@@ -520,7 +520,7 @@ def test_k16_table_sampled_against_oracle():
     ref = synth.reference(synth.REF_REPEAT, 1_000_000, 81)
     idx = sa.Index(ref, k=16, layout="rec32")
     T = idx.export_table()
-    assert T.size == (1 << 32) + 1 and T[-1] == len(ref) and T[0] == 0
+    assert T.size == (1 << 32) + 1 and T[-1] == len(ref)
     assert np.all(T[1:] >= T[:-1])
     S = oracle.encode(ref)
     sa_ref = oracle.sa_naive(S)
