@@ -13,6 +13,11 @@
 #include "sa_search_long.cuh"
 #include "sa_search_dual.cuh"
 
+// the hand-written read-ordering sort (csrc/sa_order.cu)
+size_t sa_order_onesweep_bytes(uint64_t Q);
+sa_status sa_order_onesweep(const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len, uint32_t stride,
+                            uint64_t Q, uint32_t key_bases, uint8_t *ws, uint32_t *order, cudaStream_t st);
+
 namespace {
 
 using sa_search::MatchArgs;
@@ -187,6 +192,10 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
                                                         (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)Q, 0, 32);
 #endif
         if (e != cudaSuccess) { sa_set_error("order size query: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+#ifdef SA_ORDER_ONESWEEP  // (A/B build) the hand-written sort (csrc/sa_order.cu) uses the same scratch region
+        const size_t ob = sa_order_onesweep_bytes(Q);
+        if (ob > b) b = ob;
+#endif
         L.cub = off;
         L.cub_bytes = b;
         off = align256(off + b);
@@ -221,6 +230,9 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     // 4-byte stores are partial-sector DRAM read-modify-writes: 5.6 GB written, 5.2 GB read per pass
     // for 0.8 GB of payload; CUB's 8-bit digits keep each bin's run long enough to coalesce).
     const int end_bit = 2 * (int)key_bases + (short_last ? 1 : 0);
+#ifdef SA_ORDER_ONESWEEP  // A/B build: the hand-written onesweep sort (csrc/sa_order.cu; measured slower)
+    if (!short_last) return sa_order_onesweep(q_words, q_len, fixed_len, stride, Q, key_bases, ws + L.cub, order, st);
+#endif
 #ifdef SA_ORDER_PACKED
     if (!short_last && Q < (1ull << 27)) {
         // keys_in .. perm_in hold the packed 64-bit keys; keys_out .. (+8 B) the sorted ones
