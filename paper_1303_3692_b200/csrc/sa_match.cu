@@ -12,6 +12,7 @@
 #include "sa_search.cuh"
 #include "sa_search_long.cuh"
 #include "sa_search_dual.cuh"
+#include "sa_search_staged.cuh"
 
 // the hand-written read-ordering sort (csrc/sa_order.cu)
 size_t sa_order_onesweep_bytes(uint64_t Q);
@@ -71,6 +72,51 @@ cudaError_t launch_long(const MatchArgs &a, int layout, bool stats, cudaStream_t
     case L_REC32: return stats ? launch_l<L_REC32, true>(a, st) : launch_l<L_REC32, false>(a, st);
     default: return stats ? launch_l<L_REC16, true>(a, st) : launch_l<L_REC16, false>(a, st);
     }
+}
+
+// long reads with the phase-B verification staged in shared memory by TMA (sa_search_staged.cuh)
+#ifndef SA_STAGE_WARP_BYTES
+#define SA_STAGE_WARP_BYTES 6144  // staging bytes per warp (8 warps x 6 KB = 48 KB per block, 4 blocks per SM)
+#endif
+template <int L, bool STATS>
+cudaError_t launch_s(const MatchArgs &a, uint32_t part_words, uint32_t slots, cudaStream_t st) {
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+    const size_t smem = (size_t)8 * slots * 2 * part_words * 8;
+    cudaError_t e = cudaFuncSetAttribute(sa_search::k_match_staged<L, STATS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    sa_search::k_match_staged<L, STATS><<<blocks, threads, smem, st>>>(a, part_words, slots);
+    return cudaGetLastError();
+}
+
+// the staging geometry for reads of at most m_max bases, or false when k_match<0> takes the launch (plain
+// layout: no records; reads no longer than the record-decided prefix; windows too long for the budget;
+// a read buffer that is not 16-byte aligned; SA_STAGED=0 in the environment, for A/B runs)
+bool staged_geometry(int layout, uint32_t k, uint32_t m_max, const void *words, uint32_t &part_words,
+                     uint32_t &slots) {
+    static const bool off = [] {
+        const char *e = getenv("SA_STAGED");
+        return e && e[0] == '0';
+    }();
+#ifdef SA_NO_STAGED  // A/B build (variants/libsa_nostaged.so): k_match<0> for every long read
+    return false;
+#endif
+    if (off || layout == sa_search::L_PLAIN || (reinterpret_cast<uintptr_t>(words) & 15)) return false;
+    const uint32_t mt = k + (layout == sa_search::L_REC32 ? 112u : 48u);
+    if (m_max <= mt) return false;
+    const uint32_t lmax = m_max - mt;
+    part_words = ((lmax + 31) / 32 + 4) & ~1u;
+    slots = std::min<uint32_t>(32u, SA_STAGE_WARP_BYTES / (16u * part_words));
+    return slots >= 2;
+}
+
+cudaError_t launch_staged(const MatchArgs &a, int layout, bool stats, uint32_t part_words, uint32_t slots,
+                          cudaStream_t st) {
+    using namespace sa_search;
+    if (layout == L_REC32)
+        return stats ? launch_s<L_REC32, true>(a, part_words, slots, st) : launch_s<L_REC32, false>(a, part_words, slots, st);
+    return stats ? launch_s<L_REC16, true>(a, part_words, slots, st) : launch_s<L_REC16, false>(a, part_words, slots, st);
 }
 
 template <int QW>
@@ -431,6 +477,7 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.rec = idx->rec;
     a.table = idx->table;
     a.n = idx->n;
+    a.text_words = idx->n_words;
     a.k = idx->k;
     a.words = q_words;
     a.lens = q_len;
@@ -491,9 +538,16 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
     else if (nw <= 2) e = launch_qw<2>(a, idx->layout, st_on, st);
     else if (nw <= 4) e = launch_qw<4>(a, idx->layout, st_on, st);
-#ifndef SA_LONG_WARP  // one thread per read, two phases (k_match<0>); the A/B build SA_LONG_WARP takes
-                      // k_match_long (warp-synchronous rounds, warp-cooperative text compares)
-    else if (!cooperative) e = launch_qw<0>(a, idx->layout, st_on, st);
+#ifndef SA_LONG_WARP  // one thread per read, two phases (k_match_staged, else k_match<0>); the A/B build
+                      // SA_LONG_WARP takes k_match_long (warp-synchronous rounds, warp-cooperative compares)
+    else if (!cooperative) {
+        uint32_t part_words = 0, slots = 0;
+        const uint32_t m_max = stride ? 32u * stride : fixed_len;
+        if (staged_geometry(idx->layout, idx->k, m_max, q_words, part_words, slots))
+            e = launch_staged(a, idx->layout, st_on, part_words, slots, st);
+        else
+            e = launch_qw<0>(a, idx->layout, st_on, st);
+    }
 #else
     else if (!cooperative) e = launch_long(a, idx->layout, st_on, st);
 #endif

@@ -28,6 +28,7 @@ struct MatchArgs {
     const uint4 *__restrict__ rec;      // L_REC16 (1 uint4 per suffix) / L_REC32 (2 uint4 per suffix)
     const uint32_t *__restrict__ table;
     uint64_t n;
+    uint64_t text_words;                // words of `text` (incl. the zero guard words)
     uint32_t k;
     const uint64_t *__restrict__ words;
     const uint32_t *__restrict__ lens;
@@ -623,10 +624,11 @@ __device__ __forceinline__ uint32_t tree_child(const TreeLoc &tl, uint32_t node,
     return c < (1u << tl.depth) ? c : 0u;
 }
 
+// (returns the pivot's suffix position SA[p])
 template <int L, class RD>
-__device__ __forceinline__ void probe(const MatchArgs &a, const RD &P, uint32_t m, uint64_t p,
-                                      uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts,
-                                      const TreeLoc &tl = TreeLoc{0, 0}, uint32_t node = 0) {
+__device__ __forceinline__ uint64_t probe(const MatchArgs &a, const RD &P, uint32_t m, uint64_t p,
+                                          uint32_t skip, bool in_bracket, int &sign, uint32_t &lcp, uint32_t &texts,
+                                          const TreeLoc &tl = TreeLoc{0, 0}, uint32_t node = 0) {
     Probe<L> pr;
     if constexpr (L == L_REC32) {
         if (node) pr.r.load(a.tree, tree_rec(tl, node));  // the same record, from the bucket's tree
@@ -635,6 +637,7 @@ __device__ __forceinline__ void probe(const MatchArgs &a, const RD &P, uint32_t 
         pr.load(a, p);
     }
     compare_probe(a, pr, P, m, skip, in_bracket, sign, lcp, texts);
+    return pr.sa();
 }
 
 // Binary search over (Lp1-1, R): LB rule (lower: R moves when P <= t) or RB rule (R moves when P < t).
@@ -709,14 +712,14 @@ template <int L, bool TREE, class RD>
 __device__ __forceinline__ void joint_search(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1, uint32_t R,
                                              uint32_t lcp0, const TreeLoc &tl, uint32_t node, uint32_t &lo,
                                              uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
-                                             const TreeCtx *tc);
+                                             const TreeCtx *tc, uint32_t *split_sa = nullptr);
 
 // One read: [lo, hi).  L is carried as L+1 (Lp1) so every bound fits uint32.  BT: the index may have
 // bucket trees (SA_INDEX_BUCKET_TREE; a separate instantiation keeps the default kernel's registers).
 template <int L, bool TREE = false, bool BT = false, class RD>
 __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uint32_t m, uint32_t &lo,
                                             uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
-                                            const TreeCtx *tc = nullptr) {
+                                            const TreeCtx *tc = nullptr, uint32_t *split_sa = nullptr) {
     const uint32_t k = a.k;
     auto clamp = [&](uint32_t v) { return min(max(v, a.clo), a.chi); };
     if (m == 0) {  // the empty read is a prefix of every suffix (reading A12): [0, n), clamped
@@ -778,7 +781,7 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
             }
         }
     }
-    joint_search<L, TREE>(a, P, m, Lp1, R, 0, tl, node, lo, hi, steps, texts, ubytes, tc);
+    joint_search<L, TREE>(a, P, m, Lp1, R, 0, tl, node, lo, hi, steps, texts, ubytes, tc, split_sa);
 }
 
 // The joint lo/hi search over the bracket (Lp1 - 1, R) -- every suffix in it shares P's first lcp0
@@ -787,7 +790,7 @@ template <int L, bool TREE, class RD>
 __device__ __forceinline__ void joint_search(const MatchArgs &a, const RD &P, uint32_t m, uint32_t Lp1, uint32_t R,
                                              uint32_t lcp0, const TreeLoc &tl, uint32_t node, uint32_t &lo,
                                              uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
-                                             const TreeCtx *tc) {
+                                             const TreeCtx *tc, uint32_t *split_sa) {
     uint32_t lcpL = lcp0, lcpR = lcp0;
     uint32_t hLp1 = 0, hR = 0, hlcpL = 0, hlcpR = 0, hnode = 0;
     bool split = false;
@@ -797,11 +800,12 @@ __device__ __forceinline__ void joint_search(const MatchArgs &a, const RD &P, ui
         int sign;
         uint32_t lcp;
         const uint32_t skip = min(lcpL, lcpR);
-        probe<L>(a, P, m, p, skip, true, sign, lcp, texts, tl, node);
+        const uint64_t sp = probe<L>(a, P, m, p, skip, true, sign, lcp, texts, tl, node);
         ++steps;
         ubytes += probe_bytes(m, skip, lcp);
         if (sign == 0) {  // lo lies in (L, p], hi in (p, R]: the RB search starts from here
             split = true;
+            if (split_sa) *split_sa = (uint32_t)sp;  // (the staged long-read kernel: SA[p] of the split)
             hLp1 = p + 1; hR = R; hlcpL = lcp; hlcpR = lcpR;
             R = p; lcpR = lcp;
             hnode = tree_child(tl, node, false);

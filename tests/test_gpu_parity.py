@@ -535,3 +535,53 @@ def test_k16_table_sampled_against_oracle():
     words = (xs << np.uint64(32)).reshape(-1, 1)
     want = oracle.search_batch(S, sa_ref, words, None, fixed_len=16)[:, 0]
     assert np.array_equal(T[xs.astype(np.int64)].astype(np.uint64), want)
+
+
+@pytest.mark.parametrize("layout", ["rec16", "rec32"])
+def test_staged_long_read_verification(layout):
+    """k_match_staged (reads over k + cached bases; phase (B) windows staged in shared memory by TMA bulk
+    copies, sa_search_staged.cuh) against the oracle: unique loci (one verification), a 2-kb exact
+    duplication (hi' - lo' = 2: the per-thread joint search), substitutions at the first staged base, in the
+    middle and at the last base, reads running past the end of the text (suffix shorter than the read),
+    more candidates per warp than staging slots (m = 3000: 4 slots), and the same batch through a read
+    buffer that is only 8-byte aligned (the k_match<0> fallback)."""
+    rng = random.Random(7)
+    base = synth.reference(synth.REF_REPEAT, 200_000, 91).tobytes().decode()
+    dup = base[50_000:52_000]
+    ref = base[:120_000] + dup + base[120_000:]  # the 2-kb block twice
+    n = len(ref)
+    qs = []
+    for m in [129, 140, 145, 200, 333, 500, 1000, 1500, 3000]:
+        for _ in range(40):
+            i = rng.randrange(n - m + 1)
+            s = ref[i:i + m]
+            r = rng.random()
+            if r < 0.4:
+                qs.append(s)
+            else:
+                j = rng.choice([128, 129, 144, m // 2, m - 1, rng.randrange(128, m)])
+                j = min(max(j, 0), m - 1)
+                qs.append(s[:j] + "ACGT".replace(s[j], "")[rng.randrange(3)] + s[j + 1:])
+        if m <= 2000:
+            o = 50_000 + rng.randrange(0, 2000 - m + 1)
+            qs.append(base[o:o + m])  # inside the duplication: two occurrences
+        qs.append(ref[n - m:])                                          # the last m bases
+        qs.append(ref[n - m + 10:] + "ACGTACGTAC")                      # runs past the end by 10 bases
+        qs.append(ref[n - (m - 5):] + "T" * 5)
+    words, lens = synth.pack_strings(qs)
+    S = oracle.encode(ref.encode())
+    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
+    idx = sa.Index(ref.encode(), layout=layout)
+    for offset in (0, 1):  # 1: the rows start 8 bytes past a 16-byte boundary -> k_match<0>
+        Q, stride = words.shape
+        buf = torch.zeros(Q * stride + 2, dtype=torch.int64, device="cuda")
+        w = buf[offset:offset + Q * stride].view(Q, stride)
+        w.copy_(torch.from_numpy(words.view(np.int64)))
+        l = torch.from_numpy(lens.view(np.int32)).cuda()
+        for presort in (False, True):
+            got = idx.match(w, l, presort=presort)
+            torch.cuda.synchronize()
+            got = got.cpu().numpy().view(np.uint32)
+            bad = np.nonzero((got != want).any(axis=1))[0]
+            assert bad.size == 0, f"offset {offset} presort {presort}: {bad.size} mismatches, q={bad[0]} m={lens[bad[0]]}"
+    assert (want[:, 1] - want[:, 0] == 2).any()  # the duplication was exercised
