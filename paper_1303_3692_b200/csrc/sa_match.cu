@@ -82,7 +82,7 @@ template <int L, bool STATS>
 cudaError_t launch_s(const MatchArgs &a, uint32_t part_words, uint32_t slots, cudaStream_t st) {
     const int threads = 256;
     const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
-    const size_t smem = (size_t)8 * slots * 2 * part_words * 8;
+    const size_t smem = (size_t)8 * slots * (2 * part_words + 2) * 8;
     cudaError_t e = cudaFuncSetAttribute(sa_search::k_match_staged<L, STATS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -90,25 +90,25 @@ cudaError_t launch_s(const MatchArgs &a, uint32_t part_words, uint32_t slots, cu
     return cudaGetLastError();
 }
 
-// the staging geometry for reads of at most m_max bases, or false when k_match<0> takes the launch (plain
-// layout: no records; reads no longer than the record-decided prefix; windows too long for the budget;
-// a read buffer that is not 16-byte aligned; SA_STAGED=0 in the environment, for A/B runs)
+// the staging geometry for reads of at most m_max bases, or false when k_match<0> takes the launch.  The
+// staged kernel is an A/B build (SA_MATCH_STAGED, variants/libsa_staged.so): bit-exact, but slower than
+// k_match<0> at every read length (profiles/r02/r02u), so the default build never stages.
+// (Also k_match<0>: the plain layout (no records), reads no longer than the record-decided prefix,
+// windows too long for the budget, a read buffer that is not 16-byte aligned.)
 bool staged_geometry(int layout, uint32_t k, uint32_t m_max, const void *words, uint32_t &part_words,
                      uint32_t &slots) {
-    static const bool off = [] {
-        const char *e = getenv("SA_STAGED");
-        return e && e[0] == '0';
-    }();
-#ifdef SA_NO_STAGED  // A/B build (variants/libsa_nostaged.so): k_match<0> for every long read
+#ifndef SA_MATCH_STAGED
+    (void)layout; (void)k; (void)m_max; (void)words; (void)part_words; (void)slots;
     return false;
-#endif
-    if (off || layout == sa_search::L_PLAIN || (reinterpret_cast<uintptr_t>(words) & 15)) return false;
+#else
+    if (layout == sa_search::L_PLAIN || (reinterpret_cast<uintptr_t>(words) & 15)) return false;
     const uint32_t mt = k + (layout == sa_search::L_REC32 ? 112u : 48u);
     if (m_max <= mt) return false;
     const uint32_t lmax = m_max - mt;
     part_words = ((lmax + 31) / 32 + 4) & ~1u;
-    slots = std::min<uint32_t>(32u, SA_STAGE_WARP_BYTES / (16u * part_words));
+    slots = std::min<uint32_t>(32u, SA_STAGE_WARP_BYTES / (8u * (2u * part_words + 2u)));
     return slots >= 2;
+#endif
 }
 
 cudaError_t launch_staged(const MatchArgs &a, int layout, bool stats, uint32_t part_words, uint32_t slots,

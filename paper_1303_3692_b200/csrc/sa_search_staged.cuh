@@ -72,14 +72,17 @@ __device__ __forceinline__ uint64_t stage_word(const uint64_t *d, uint32_t i, ui
 #endif
 
 // part_words: words of one window's staging area (>= ceil(Lmax/32) + 3, even); slots: windows pairs
-// per warp.  Dynamic shared memory: 8 warps x slots x 2 x part_words x 8 bytes.
+// per warp.  Dynamic shared memory: 8 warps x slots x (2 x part_words + 2) x 8 bytes.
 template <int L, bool STATS>
 __global__ void __launch_bounds__(256, SA_STAGED_MINB) k_match_staged(const MatchArgs a, uint32_t part_words,
                                                                     uint32_t slots) {
     extern __shared__ __align__(128) uint64_t s_stage[];
     __shared__ __align__(8) uint64_t s_bar[8];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t *wbuf = s_stage + (uint64_t)warp * slots * 2 * part_words;
+    // a slot = the read window (part_words) + the text window (part_words) + 2 pad words: the slot stride is
+    // 2 mod 4 words, so the lanes' 8-byte reads at equal offsets spread over the banks (2-way at most)
+    const uint32_t sw = 2 * part_words + 2;
+    uint64_t *wbuf = s_stage + (uint64_t)warp * slots * sw;
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar[warp]);
     if (lane == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(256, SA_STAGED_MINB) k_match_staged(const Matc
         pending = rest;
         const bool mine = (sel >> lane) & 1u;
         const uint32_t slot = __popc(sel & ((1u << lane) - 1u));
-        uint64_t *rs = wbuf + (uint64_t)slot * 2 * part_words, *ts = rs + part_words;
+        uint64_t *rs = wbuf + (uint64_t)slot * sw, *ts = rs + part_words;
         StageWin gr{0, 0, 0, 0}, gt{0, 0, 0, 0};
         uint32_t bytes = 0;
         if (mine && Lc) {
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(256, SA_STAGED_MINB) k_match_staged(const Matc
         }
         phase ^= 1u;
         __syncwarp();  // (the plain-load tail words of every lane are visible to the warp)
+#ifdef SA_STAGED_WARPCMP  // A/B: each selected lane's window pair compared by the whole warp (lane j: word j)
         for (uint32_t s2 = sel; s2;) {  // each selected lane's window pair, compared by the whole warp
             const int o = __ffs(s2) - 1;
             s2 &= s2 - 1;
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(256, SA_STAGED_MINB) k_match_staged(const Matc
             const uint32_t oL = __shfl_sync(0xFFFFFFFFu, Lc, o);
             const uint32_t roff = __shfl_sync(0xFFFFFFFFu, gr.off, o), rsh = __shfl_sync(0xFFFFFFFFu, gr.sh, o);
             const uint32_t toff = __shfl_sync(0xFFFFFFFFu, gt.off, o), tsh = __shfl_sync(0xFFFFFFFFu, gt.sh, o);
-            const uint64_t *R = wbuf + (uint64_t)v * 2 * part_words, *T = R + part_words;
+            const uint64_t *R = wbuf + (uint64_t)v * sw, *T = R + part_words;
             const uint32_t nwL = (oL + 31) >> 5;
             int fsg = 0;
             uint32_t flc = 0xFFFFFFFFu;
@@ -183,6 +187,25 @@ __global__ void __launch_bounds__(256, SA_STAGED_MINB) k_match_staged(const Matc
                 else { vsign = 1; vlcp = (uint32_t)slen; }             // the suffix is a proper prefix of P (A7)
             }
         }
+#else  // each selected lane compares its own window pair from shared memory, 32 bases per step
+        if (mine) {
+            const uint32_t nwL = (Lc + 31) >> 5;
+            uint32_t j = 0;
+            for (; j < nwL; ++j) {
+                const uint64_t mask = prefix_mask(min(32u, Lc - 32u * j));
+                const uint64_t x = stage_word(rs, gr.off + j, gr.sh) & mask, y = stage_word(ts, gt.off + j, gt.sh) & mask;
+                if (x != y) {
+                    vlcp = mt + 32u * j + ((uint32_t)__clzll((long long)(x ^ y)) >> 1);
+                    vsign = x > y ? 1 : -1;
+                    break;
+                }
+            }
+            if (j == nwL) {
+                if (m <= slen) { vsign = 0; vlcp = m; }           // P is a prefix of the suffix
+                else { vsign = 1; vlcp = (uint32_t)slen; }        // the suffix is a proper prefix of P (A7)
+            }
+        }
+#endif
         __syncwarp();
     }
     if (valid) {

@@ -539,8 +539,9 @@ def test_k16_table_sampled_against_oracle():
 
 @pytest.mark.parametrize("layout", ["rec16", "rec32"])
 def test_staged_long_read_verification(layout):
-    """k_match_staged (reads over k + cached bases; phase (B) windows staged in shared memory by TMA bulk
-    copies, sa_search_staged.cuh) against the oracle: unique loci (one verification), a 2-kb exact
+    """The long-read kernel (k_match<0>; with SA_LIB_PATH=variants/libsa_staged.so k_match_staged, whose
+    phase (B) windows are staged in shared memory by TMA bulk copies, sa_search_staged.cuh) against the
+    oracle: unique loci (one verification), a 2-kb exact
     duplication (hi' - lo' = 2: the per-thread joint search), substitutions at the first staged base, in the
     middle and at the last base, reads running past the end of the text (suffix shorter than the read),
     more candidates per warp than staging slots (m = 3000: 4 slots), and the same batch through a read
