@@ -39,6 +39,7 @@ import synth  # noqa: E402
 
 METRIC = "exact-match queries/sec and achieved HBM GB/s at 1/2/4/8 B200"
 UNIT = "queries/s"
+BUCKET_MAX_Q = 16_000_000  # order_method auto: bucket placement up to this many reads per GPU
 
 
 def log(*a):
@@ -74,6 +75,9 @@ def parse():
     ap.add_argument("--tree", action="store_true",
                     help="time the flattened suffix tree walk (sa_tree_match, SURVEY.md 8(f) f3) instead of the SA search")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
+    ap.add_argument("--order-method", choices=["auto", "sort", "buckets"], default="sort",
+                    help="read ordering: the stable radix sort, bucket placement (SA_ORDER_BUCKETS), or auto "
+                         "(buckets when the rank's batch is <= BUCKET_MAX_Q reads)")
     ap.add_argument("--rows-ordered", action="store_true",
                     help="the ordering step also gathers the read rows into order (SA_MATCH_ROWS_ORDERED)")
     ap.add_argument("--cooperative", action="store_true",
@@ -416,7 +420,12 @@ def main():
 
     stream = torch.cuda.current_stream()
     presort = not args.no_order
-    ws = torch.empty(max(1, idx.workspace_size(Q, stride, sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT)),
+    # the read ordering (a5): the stable radix sort, or bucket placement (SA_ORDER_BUCKETS) for batches
+    # whose permutation + 4^12 counters stay in L2 ("auto": Q <= BUCKET_MAX_Q reads per GPU)
+    buckets = presort and (args.order_method == "buckets" or
+                           (args.order_method == "auto" and Q <= BUCKET_MAX_Q and args.order_bases <= 12))
+    ws = torch.empty(max(1, idx.workspace_size(Q, stride, sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT),
+                         idx.order_workspace_size(Q, args.order_bases, buckets=buckets)),
                      dtype=torch.uint8, device=dev)
     perm = torch.empty(Q, dtype=torch.int32, device=dev) if presort else None
     rows_ordered = presort and args.rows_ordered
@@ -456,7 +465,7 @@ def main():
             return
         if presort:
             idx.order(words, lens, fixed_len=fixed, out=perm, stream=stream, workspace=ws, key_bases=args.order_bases,
-                      ordered_words=owords, ordered_lens=olens)
+                      ordered_words=owords, ordered_lens=olens, buckets=buckets)
         if i is not None:
             ev[i][0].record(stream)
         if tree is not None:
@@ -483,7 +492,8 @@ def main():
         cs = torch.cuda.Stream(device=dev)
         cs.wait_stream(stream)
         with torch.cuda.graph(g_order, stream=cs):
-            idx.order(words, lens, fixed_len=fixed, out=perm, stream=cs, workspace=ws, key_bases=args.order_bases)
+            idx.order(words, lens, fixed_len=fixed, out=perm, stream=cs, workspace=ws, key_bases=args.order_bases,
+                      buckets=buckets)
         with torch.cuda.graph(g_match, stream=cs):
             idx.match(words, lens, fixed_len=fixed, out=out, stream=cs, workspace=ws, order=perm,
                       smem_tree=args.smem_tree, tree_key_bases=args.order_bases)
@@ -540,9 +550,11 @@ def main():
             "config": config_json(cfg, world, Q, weak=args.weak, k=idx.k, index_bytes=idx.device_bytes),
             "numa": numa,
             "clocks": sampler.result(),
-            "gpu_launches": args.steps * (2 if presort else 1),
-            "library_launches_per_step": (f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
+            "gpu_launches": args.steps * ((3 if buckets else 2) if presort else 1),
+            "library_launches_per_step": ("CUB exclusive scan of the 4^key_bases bucket counters" if buckets else
+                                          f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
                                           if presort else 0),
+            "order_method": ("buckets (SA_ORDER_BUCKETS)" if buckets else "stable radix sort") if presort else None,
             "launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
             "shards": summary_all, "layout": args.layout, "smem_tree_levels": args.smem_tree,
             "bucket_tree": args.bucket_tree, "cuda_graphs": graphs is not None, "read_order": f"sorted by first {args.order_bases} bases (sa_match_order, timed)" if presort else "as given",

@@ -176,7 +176,16 @@ sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words, const uin
  * paper's "coalesced binary search".  Requires Q < 2^32.
  * ordered_words (dev, Q*stride_words, nullable) / ordered_len (dev, Q, nullable): if given, also
  * receive the reads' rows / lengths in that order (row t = read order[t]), for SA_MATCH_ROWS_ORDERED. */
+/* key_bases flag: order by bucket placement instead of the stable radix sort -- one count pass,
+ * one scan over 4^key_bases counters, one placement pass (an atomic slot claim per bucket).  The
+ * buckets come out in the same key order; reads with EQUAL keys are in no fixed order (not stable,
+ * not reproducible between calls).  Results of sa_match_batch never depend on the order.  Meant for
+ * batches whose permutation and counters fit the 126 MB L2 (e.g. Q <= 16 M at key_bases = 12);
+ * key_bases <= 13.  Workspace: sa_match_order_workspace_size_ex(Q, key_bases | SA_ORDER_BUCKETS). */
+#define SA_ORDER_BUCKETS 0x100u
 sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes);
+/* The workspace of sa_match_order for these key_bases (with or without SA_ORDER_BUCKETS). */
+sa_status sa_match_order_workspace_size_ex(uint64_t Q, uint32_t key_bases, size_t *bytes);
 sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                          uint32_t stride_words, uint64_t Q, uint32_t key_bases, uint32_t *order,
                          uint64_t *ordered_words, uint32_t *ordered_len, void *workspace, size_t ws_bytes,

@@ -28,6 +28,7 @@ SA_MATCH_PRESORT = 4        # sa_match_batch flags: order reads by their first 1
 SA_MATCH_ROWS_ORDERED = 8   # sa_match_batch flags: rows already arranged in `order` order
 SA_MATCH_COOPERATIVE = 32   # sa_match_batch flags: reads over 128 bases searched by 8/16/32-lane groups
 SA_MATCH_SMEM_TREE = 64     # sa_match_batch flags: shared-memory top tree per CTA (needs an order)
+SA_ORDER_BUCKETS = 0x100    # sa_match_order key_bases flag: bucket placement (not stable), for L2-sized batches
 SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 SA_INDEX_SUBTABLE = 8       # sa_index_opts.flags: (k+4)-base sub-tables for buckets of > 32 suffixes
 SA_INDEX_BUCKET_TREE = 16   # sa_index_opts.flags: line-packed binary-search trees for buckets of >= 32 suffixes
@@ -55,6 +56,7 @@ _SIGS = {
     "sa_match_workspace_size": ([_p, _u64, _u32, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_match_batch": ([_p, _p, _p, _u32, _u32, _u64, _p, _p, _p, _sz, _u32, _p], ctypes.c_int),
     "sa_match_order_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
+    "sa_match_order_workspace_size_ex": ([_u64, _u32, ctypes.POINTER(_sz)], ctypes.c_int),
     "sa_match_order": ([_p, _p, _p, _u32, _u32, _u64, _u32, _p, _p, _p, _p, _sz, _p], ctypes.c_int),
     "sa_match_batch_host": ([_p, _p, _p, _u32, _u32, _u64, _p, _u64], ctypes.c_int),
     "sa_locate_workspace_size": ([_u64, ctypes.POINTER(_sz)], ctypes.c_int),
@@ -275,27 +277,31 @@ class Index:
         _check(lib().sa_match_workspace_size(self._h, Q, stride, flags, ctypes.byref(ws)), "sa_match_workspace_size")
         return ws.value
 
-    def order_workspace_size(self, Q: int) -> int:
+    def order_workspace_size(self, Q: int, key_bases: int = 0, buckets: bool = False) -> int:
         ws = _sz()
-        _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(ws)), "sa_match_order_workspace_size")
+        kb = int(key_bases) | (SA_ORDER_BUCKETS if buckets else 0)
+        _check(lib().sa_match_order_workspace_size_ex(Q, kb, ctypes.byref(ws)), "sa_match_order_workspace_size_ex")
         return ws.value
 
     def order(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, workspace=None,
-              key_bases: int = 0, ordered_words=None, ordered_lens=None, n_reads: Optional[int] = None):
+              key_bases: int = 0, ordered_words=None, ordered_lens=None, n_reads: Optional[int] = None,
+              buckets: bool = False):
         """sa_match_order: a permutation of the reads sorted by their first key_bases bases (0 = 12);
         optionally also the rows / lengths arranged in that order (for match(..., rows_ordered=True)).
-        n_reads: give it (with a 1-D `words` stream and fixed_len) for the dense layout."""
+        n_reads: give it (with a 1-D `words` stream and fixed_len) for the dense layout.
+        buckets: SA_ORDER_BUCKETS (bucket placement; equal keys in no fixed order)."""
         import torch
         Q, stride = _rows(words, n_reads)
+        kb = int(key_bases) | (SA_ORDER_BUCKETS if buckets else 0)
         need = _sz()
-        _check(lib().sa_match_order_workspace_size(Q, ctypes.byref(need)), "sa_match_order_workspace_size")
+        _check(lib().sa_match_order_workspace_size_ex(Q, kb, ctypes.byref(need)), "sa_match_order_workspace_size_ex")
         if workspace is None or workspace.numel() < need.value:
             workspace = _empty(max(1, need.value), torch.uint8, words.device, stream)
         if out is None:
             out = _empty(Q, torch.int32, words.device, stream)
-        _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, int(key_bases),
+        _check(lib().sa_match_order(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, kb,
                                     _dptr(out), _dptr(ordered_words), _dptr(ordered_lens), _dptr(workspace),
-                                    need.value, _stream_ptr(stream)), "sa_match_order")
+                                    workspace.numel(), _stream_ptr(stream)), "sa_match_order")
         return out
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,

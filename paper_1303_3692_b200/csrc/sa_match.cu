@@ -251,6 +251,7 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
 }
 
 constexpr uint32_t kDefaultKeyBases = 12;
+constexpr uint32_t kMaxBucketBases = 13;  // SA_ORDER_BUCKETS: at most 4^13 counters (256 MB)
 
 #ifdef SA_ORDER_PACKED
 // the sorted packed keys (key << 27 | read index) -> the permutation
@@ -298,6 +299,103 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     SA_CUDA_TRY(cudaGetLastError());
     SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0,
                                                 end_bit, st));
+    return SA_OK;
+}
+
+// ---- bucket order (SA_ORDER_BUCKETS) ------------------------------------------------------------
+// One placement pass instead of a radix sort: every read goes to the bucket of its first key_bases
+// bases (4^key_bases buckets): count (k_bucket_count), exclusive scan of the counts (CUB), place
+// (k_bucket_place: a slot claimed by an atomic on the bucket's offset).  The buckets come out in key
+// order, as with the sort; inside a bucket the reads are in no fixed order (lanes of a warp with the same
+// key claim their slots together, in lane order, after one __match_any_sync).  For batches whose
+// permutation and counters stay in the 126 MB L2, so the scattered 4-byte slot writes and the counter
+// atomics merge there instead of becoming partial-sector DRAM read-modify-writes (the reason the
+// round-1 counting sorts lost at 100 M reads, order_reads).
+__device__ __forceinline__ uint32_t read_key(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens,
+                                             uint32_t fixed_len, uint32_t stride, uint64_t dense_words, uint64_t q,
+                                             uint32_t key_bases) {
+    uint32_t m;
+    uint64_t w0;
+    if (stride == 0) {
+        m = fixed_len;
+        const uint64_t bit = 2ull * m * q, i = bit >> 6;
+        const unsigned sh = (unsigned)(bit & 63);
+        const uint64_t lo = __ldg(reinterpret_cast<const unsigned long long *>(words) + i);
+        const uint64_t hi = (sh && i + 1 < dense_words) ? __ldg(reinterpret_cast<const unsigned long long *>(words) + i + 1) : 0ull;
+        w0 = sh ? (lo << sh) | (hi >> (64 - sh)) : lo;
+    } else {
+        m = min(lens ? __ldg(lens + q) : fixed_len, 32u * stride);
+        w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
+    }
+    return (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases));
+}
+
+__global__ void k_bucket_count(const uint64_t *__restrict__ words, const uint32_t *__restrict__ lens, uint32_t fixed_len,
+                               uint32_t stride, uint64_t dense_words, uint64_t Q, uint32_t key_bases,
+                               uint32_t *__restrict__ keys, uint32_t *__restrict__ cnt) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = q < Q;
+    const uint32_t key = ok ? read_key(words, lens, fixed_len, stride, dense_words, q, key_bases) : 0xFFFFFFFFu;
+    if (ok) keys[q] = key;
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, ok);
+    if (!ok) return;
+    const unsigned peers = __match_any_sync(act, key);  // (repeats: many reads share a key)
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(cnt + key, (uint32_t)__popc(peers));
+}
+
+__global__ void k_bucket_place(const uint32_t *__restrict__ keys, uint64_t Q, uint32_t *__restrict__ off,
+                               uint32_t *__restrict__ order) {
+    const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = q < Q;
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, ok);
+    if (!ok) return;
+    const uint32_t key = keys[q];
+    const unsigned peers = __match_any_sync(act, key);
+    const unsigned lane = threadIdx.x & 31, leader = (unsigned)(__ffs(peers) - 1);
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(off + key, (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, (int)leader);
+    order[base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)q;
+}
+
+struct BucketLayout {
+    size_t keys = 0, cnt = 0, off = 0, scan = 0, scan_bytes = 0, total = 0;
+};
+
+sa_status bucket_layout(uint64_t Q, uint32_t key_bases, BucketLayout &B) {
+    if (key_bases > kMaxBucketBases) {
+        sa_set_error("SA_ORDER_BUCKETS: key_bases %u > %u", key_bases, kMaxBucketBases);
+        return SA_EINVAL;
+    }
+    const uint64_t nb = 1ull << (2 * key_bases);
+    size_t o = 0;
+    B.keys = o; o = align256(o + Q * 4);
+    B.cnt = o; o = align256(o + nb * 4);
+    B.off = o; o = align256(o + nb * 4);
+    size_t b = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nb);
+    if (e != cudaSuccess) { sa_set_error("scan size query: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+    B.scan = o; B.scan_bytes = b; o = align256(o + b);
+    B.total = o;
+    return SA_OK;
+}
+
+sa_status order_buckets(const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len, uint32_t stride, uint64_t Q,
+                        uint32_t key_bases, uint8_t *ws, const BucketLayout &B, uint32_t *order, cudaStream_t st) {
+    const uint64_t nb = 1ull << (2 * key_bases);
+    uint32_t *keys = reinterpret_cast<uint32_t *>(ws + B.keys);
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(ws + B.cnt);
+    uint32_t *off = reinterpret_cast<uint32_t *>(ws + B.off);
+    const uint64_t dense_words = (Q * (uint64_t)fixed_len + 31) / 32;
+    const uint64_t blocks = (Q + 255) / 256;
+    if (blocks > 0x7FFFFFFFull) { sa_set_error("SA_ORDER_BUCKETS: Q too large"); return SA_EINVAL; }
+    SA_CUDA_TRY(cudaMemsetAsync(cnt, 0, nb * 4, st));
+    k_bucket_count<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases, keys, cnt);
+    SA_CUDA_TRY(cudaGetLastError());
+    size_t b = B.scan_bytes;
+    SA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ws + B.scan, b, cnt, off, (int64_t)nb, st));
+    k_bucket_place<<<(unsigned)blocks, 256, 0, st>>>(keys, Q, off, order);
+    SA_CUDA_TRY(cudaGetLastError());
     return SA_OK;
 }
 
@@ -432,24 +530,50 @@ extern "C" sa_status sa_match_order_workspace_size(uint64_t Q, size_t *bytes) {
     return SA_OK;
 }
 
+extern "C" sa_status sa_match_order_workspace_size_ex(uint64_t Q, uint32_t key_bases, size_t *bytes) {
+    sa_clear_error();
+    if (!bytes) { sa_set_error("NULL argument"); return SA_EINVAL; }
+    if (!(key_bases & SA_ORDER_BUCKETS)) return sa_match_order_workspace_size(Q, bytes);
+    uint32_t kb = key_bases & 0xFFu;
+    if (kb == 0) kb = kDefaultKeyBases;
+    BucketLayout B;
+    SA_TRY(bucket_layout(Q, kb, B));
+    *bytes = B.total;
+    return SA_OK;
+}
+
 extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len,
                                     uint32_t fixed_len, uint32_t stride_words, uint64_t Q, uint32_t key_bases,
                                     uint32_t *order, uint64_t *ordered_words, uint32_t *ordered_len,
                                     void *workspace, size_t ws_bytes, void *stream) {
     sa_clear_error();
+    const bool buckets = (key_bases & SA_ORDER_BUCKETS) != 0;
+    key_bases &= ~SA_ORDER_BUCKETS;
     if (key_bases > 16) { sa_set_error("key_bases %u > 16", key_bases); return SA_EINVAL; }
     if (key_bases == 0) key_bases = kDefaultKeyBases;
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, order));
     if (Q == 0) return SA_OK;
     SA_CUDA_TRY(cudaSetDevice(idx->device));
-    PresortLayout L;
-    SA_TRY(presort_layout(Q, false, true, true, L));
-    if (!workspace || ws_bytes < L.total) {
-        sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
-        return SA_EINVAL;
+    if (buckets) {
+        if (Q >= (1ull << 32)) { sa_set_error("read ordering needs Q < 2^32"); return SA_EINVAL; }
+        BucketLayout B;
+        SA_TRY(bucket_layout(Q, key_bases, B));
+        if (!workspace || ws_bytes < B.total) {
+            sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, B.total);
+            return SA_EINVAL;
+        }
+        SA_TRY(order_buckets(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace),
+                             B, order, (cudaStream_t)stream));
+    } else {
+        PresortLayout L;
+        SA_TRY(presort_layout(Q, false, true, true, L));
+        if (!workspace || ws_bytes < L.total) {
+            sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
+            return SA_EINVAL;
+        }
+        SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace), L,
+                           order, (cudaStream_t)stream));
     }
-    SA_TRY(order_reads(q_words, q_len, fixed_len, stride_words, Q, key_bases, static_cast<uint8_t *>(workspace), L,
-                       order, (cudaStream_t)stream));
     if ((ordered_words || ordered_len) && stride_words == 0) {
         sa_set_error("ordered rows are not available for the dense layout");
         return SA_EINVAL;

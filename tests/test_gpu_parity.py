@@ -320,6 +320,54 @@ def test_order_is_a_sorted_permutation_and_keeps_results(key_bases):
     assert torch.equal(got2, base)
 
 
+@pytest.mark.parametrize("key_bases", [0, 6, 13])
+@pytest.mark.parametrize("dense", [False, True])
+def test_order_buckets_is_a_key_sorted_permutation(key_bases, dense):
+    """SA_ORDER_BUCKETS: the same bucket (key) order as the stable sort, equal keys in any order; the match
+    through that order equals the oracle.  Repeat-rich reads (thousands share a key: the warp-aggregated slot
+    claims), reads shorter than the key (masked keys), Q not a multiple of the warp, the dense layout."""
+    ref = synth.reference(synth.REF_REPEAT, 1_000_000, 61)
+    rng = np.random.default_rng(5)
+    if dense:  # equal lengths; rebuilt from strings so both layouts hold the same reads
+        m = 50
+        w0, l0 = synth.reads(ref, 30_000, m, m, 0.1, 0.0, 62)
+        qs = [synth.unpack_read(w0[i], m) for i in range(len(l0))] + ["A" * m] * 3000 + [("ACGT" * 20)[:m]] * 500
+        qs = [qs[i] for i in rng.permutation(len(qs))]
+        words, lens = synth.pack_strings(qs)
+        dense_words = synth.pack_dense(qs)
+    else:
+        words, lens = synth.reads(ref, 77_777, 3, 100, 0.1, 0.0, 62)
+        hot, hl = synth.pack_strings(["A" * 40] * 3000 + ["ACGTACGTACGTAC"] * 500, stride=words.shape[1])
+        words = np.concatenate([words, hot])
+        lens = np.concatenate([lens, hl])
+        p = rng.permutation(len(lens))
+        words, lens = np.ascontiguousarray(words[p]), np.ascontiguousarray(lens[p])
+    Q = len(lens)
+    idx = sa.Index(ref, k=12)
+    S = oracle.encode(ref)
+    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
+    kb = key_bases or 12
+    key = (words[:, 0] >> np.uint64(64 - 2 * kb)).astype(np.uint64)
+    mm = lens.astype(np.uint64)
+    short = mm < kb
+    key[short] &= ~((np.uint64(1) << (np.uint64(2) * (np.uint64(kb) - mm[short]))) - np.uint64(1))
+    if dense:
+        dw = torch.from_numpy(dense_words.view(np.int64)).cuda()
+        order = idx.order(dw, None, fixed_len=m, key_bases=key_bases, n_reads=Q, buckets=True)
+        got = idx.match(dw, None, fixed_len=m, order=order, n_reads=Q)
+    else:
+        w = torch.from_numpy(words.view(np.int64)).cuda()
+        l = torch.from_numpy(lens.view(np.int32)).cuda()
+        order = idx.order(w, l, key_bases=key_bases, buckets=True)
+        got = idx.match(w, l, order=order)
+    torch.cuda.synchronize()
+    o = order.cpu().numpy().view(np.uint32)
+    assert np.array_equal(np.sort(o), np.arange(Q, dtype=np.uint32))
+    ks = key[o]
+    assert np.all(ks[1:] >= ks[:-1])
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), want)
+
+
 @pytest.mark.parametrize("layout", ["rec16", "rec32"])
 @pytest.mark.parametrize("k", [0, 8, 12])
 @pytest.mark.parametrize("levels", [1, 5, 8, 12])
