@@ -877,6 +877,9 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
         // text compares of (B) run with the warp's lanes together instead of one by one (ncu r02c: the
         // one-phase kernel ran its text loop with 6 of 32 lanes active).
         const uint32_t mt = min(m, a.k + Rec<L>::kBases);
+        // (A direct compare for a unique P' against (A)'s split pivot -- skipping the joint search's reload
+        // of that record -- measured slower: 8.34 / 11.52 vs 8.16 / 10.87 ms per 50 M reads at m = 150 /
+        // 500, profiles/r02/r02w: the unique and the repeat lanes of a warp then run apart.)
         search_read<L, false, BT>(a, P, mt, lo, hi, steps, texts, ubytes);
         __syncwarp();
         if (m > mt) {
