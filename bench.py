@@ -75,6 +75,9 @@ def parse():
     ap.add_argument("--tree", action="store_true",
                     help="time the flattened suffix tree walk (sa_tree_match, SURVEY.md 8(f) f3) instead of the SA search")
     ap.add_argument("--order-bases", type=int, default=12, help="bases of the read-ordering key (1..16)")
+    ap.add_argument("--defer", type=int, default=0,
+                    help="SA_MATCH_DEFER: reads whose k-mer bracket holds more than 2^DEFER suffixes are searched "
+                         "in a second, full-warp pass (0 = off)")
     ap.add_argument("--order-method", choices=["auto", "sort", "buckets"], default="sort",
                     help="read ordering: the stable radix sort, bucket placement (SA_ORDER_BUCKETS), or auto "
                          "(buckets when the rank's batch is <= BUCKET_MAX_Q reads)")
@@ -425,6 +428,7 @@ def main():
     buckets = presort and (args.order_method == "buckets" or
                            (args.order_method == "auto" and Q <= BUCKET_MAX_Q and args.order_bases <= 12))
     ws = torch.empty(max(1, idx.workspace_size(Q, stride, sa.SA_MATCH_STATS | sa.SA_MATCH_PRESORT),
+                         idx.workspace_size(Q, stride, sa.SA_MATCH_PRESORT | sa.SA_MATCH_DEFER),
                          idx.order_workspace_size(Q, args.order_bases, buckets=buckets)),
                      dtype=torch.uint8, device=dev)
     perm = torch.empty(Q, dtype=torch.int32, device=dev) if presort else None
@@ -475,7 +479,8 @@ def main():
                       cooperative=args.cooperative)
         else:
             idx.match(words, lens, fixed_len=fixed, out=out, stream=stream, workspace=ws, order=perm,
-                      cooperative=args.cooperative, smem_tree=args.smem_tree, tree_key_bases=args.order_bases)
+                      cooperative=args.cooperative, smem_tree=args.smem_tree, tree_key_bases=args.order_bases,
+                      defer=args.defer)
         if i is not None:
             ev[i][1].record(stream)
 
@@ -496,7 +501,7 @@ def main():
                       buckets=buckets)
         with torch.cuda.graph(g_match, stream=cs):
             idx.match(words, lens, fixed_len=fixed, out=out, stream=cs, workspace=ws, order=perm,
-                      smem_tree=args.smem_tree, tree_key_bases=args.order_bases)
+                      smem_tree=args.smem_tree, tree_key_bases=args.order_bases, defer=args.defer)
         stream.wait_stream(cs)
         graphs = (g_order, g_match)
 
@@ -550,7 +555,8 @@ def main():
             "config": config_json(cfg, world, Q, weak=args.weak, k=idx.k, index_bytes=idx.device_bytes),
             "numa": numa,
             "clocks": sampler.result(),
-            "gpu_launches": args.steps * ((3 if buckets else 2) if presort else 1),
+            "gpu_launches": args.steps * ((3 if buckets else 2) if presort else 1) + (args.steps if args.defer else 0),
+            "defer_log2": args.defer,
             "library_launches_per_step": ("CUB exclusive scan of the 4^key_bases bucket counters" if buckets else
                                           f"CUB onesweep radix sort ({(2 * args.order_bases + 7) // 8} passes)"
                                           if presort else 0),

@@ -119,6 +119,13 @@ typedef struct {
                                    before its own probes.  L = SA_MATCH_TREE_LEVELS (1..12, 0 = 8); the
                                    key length of the order = SA_MATCH_TREE_KEY_BASES (0 = 12).  Record
                                    layouts, reads of <= 128 bases, no sub-tables.  Same results. */
+/* sa_match_batch flag: reads of <= 128 bases in two passes -- every read whose k-mer bracket holds at
+ * most 2^SA_MATCH_DEFER_LOG2 (default 8) suffixes first, the others (repeats) deferred to a second pass
+ * that searches them with full warps -- so a warp's lanes are not held by one slow repeat read.  Same
+ * results.  Workspace: sa_match_workspace_size with this flag (12 B per query more).  Not with
+ * SA_MATCH_ROWS_ORDERED, SA_MATCH_STATS or SA_MATCH_SMEM_TREE. */
+#define SA_MATCH_DEFER (1u << 17)
+#define SA_MATCH_DEFER_LOG2(b) (((uint32_t)(b) & 15u) << 18)
 #define SA_MATCH_TREE_LEVELS(l) (((uint32_t)(l) & 15u) << 8)
 #define SA_MATCH_TREE_KEY_BASES(b) (((uint32_t)(b) & 31u) << 12)
 

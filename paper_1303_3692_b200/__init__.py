@@ -29,6 +29,7 @@ SA_MATCH_ROWS_ORDERED = 8   # sa_match_batch flags: rows already arranged in `or
 SA_MATCH_COOPERATIVE = 32   # sa_match_batch flags: reads over 128 bases searched by 8/16/32-lane groups
 SA_MATCH_SMEM_TREE = 64     # sa_match_batch flags: shared-memory top tree per CTA (needs an order)
 SA_ORDER_BUCKETS = 0x100    # sa_match_order key_bases flag: bucket placement (not stable), for L2-sized batches
+SA_MATCH_DEFER = 1 << 17    # sa_match_batch flags: reads in big k-mer buckets deferred to a second full-warp pass
 SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 SA_INDEX_SUBTABLE = 8       # sa_index_opts.flags: (k+4)-base sub-tables for buckets of > 32 suffixes
 SA_INDEX_BUCKET_TREE = 16   # sa_index_opts.flags: line-packed binary-search trees for buckets of >= 32 suffixes
@@ -306,7 +307,8 @@ class Index:
 
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
               presort: bool = False, workspace=None, order=None, rows_ordered: bool = False,
-              n_reads: Optional[int] = None, cooperative: bool = False, smem_tree: int = 0, tree_key_bases: int = 0):
+              n_reads: Optional[int] = None, cooperative: bool = False, smem_tree: int = 0, tree_key_bases: int = 0,
+              defer: int = 0):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
@@ -317,6 +319,8 @@ class Index:
         n_reads: with a 1-D `words` stream and fixed_len: the dense layout (include/sa.h).
         cooperative: SA_MATCH_COOPERATIVE (reads over 128 bases: 8/16/32 lanes per read).
         smem_tree: L > 0 selects SA_MATCH_SMEM_TREE with L levels (tree_key_bases: the order's key length).
+        defer: b > 0 selects SA_MATCH_DEFER: reads whose k-mer bracket holds more than 2^b suffixes go to a
+        second pass.
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [2, Q]: row 0 steps | text windows << 16, row 1 the
@@ -336,8 +340,10 @@ class Index:
                 (SA_MATCH_ROWS_ORDERED if rows_ordered else 0) | (SA_MATCH_COOPERATIVE if cooperative else 0)
         if smem_tree:  # levels of the shared-memory top tree (include/sa.h SA_MATCH_SMEM_TREE)
             flags |= SA_MATCH_SMEM_TREE | ((int(smem_tree) & 15) << 8) | ((int(tree_key_bases) & 31) << 12)
+        if defer:
+            flags |= SA_MATCH_DEFER | ((int(defer) & 15) << 18)
         need = self.workspace_size(Q, stride, flags) \
-            if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT) else 0
+            if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_DEFER) else 0
         if need and (workspace is None or workspace.numel() < need):
             workspace = _empty(need, torch.uint8, words.device, stream)
         _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),

@@ -145,6 +145,36 @@ cudaError_t launch_group(const MatchArgs &a, int layout, bool stats, cudaStream_
     }
 }
 
+// SA_MATCH_DEFER: the light pass over all slots, then the deferred reads (grid-stride, one wave)
+template <int QW, int L>
+cudaError_t launch_defer_t(const MatchArgs &a, uint32_t big, uint32_t *dq, uint2 *dbr, uint32_t *dcount,
+                           cudaStream_t st) {
+    const int threads = SA_MATCH_THREADS;
+    const unsigned blocks = (unsigned)((a.Q + threads - 1) / threads);
+    cudaError_t e = cudaMemsetAsync(dcount, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    sa_search::k_match_light<QW, L><<<blocks, threads, 0, st>>>(a, big, dq, dbr, dcount);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned hb = (unsigned)std::min<uint64_t>(blocks, (uint64_t)sms * SA_MATCH_MINB);
+    sa_search::k_match_heavy<QW, L><<<hb, threads, 0, st>>>(a, dq, dbr, dcount);
+    return cudaGetLastError();
+}
+
+template <int QW>
+cudaError_t launch_defer(const MatchArgs &a, int layout, uint32_t big, uint32_t *dq, uint2 *dbr, uint32_t *dcount,
+                         cudaStream_t st) {
+    using namespace sa_search;
+    switch (layout) {
+    case L_PLAIN: return launch_defer_t<QW, L_PLAIN>(a, big, dq, dbr, dcount, st);
+    case L_REC32: return launch_defer_t<QW, L_REC32>(a, big, dq, dbr, dcount, st);
+    default: return launch_defer_t<QW, L_REC16>(a, big, dq, dbr, dcount, st);
+    }
+}
+
 template <int QW>
 cudaError_t launch_qw(const MatchArgs &a, int layout, bool stats, cudaStream_t st) {
     using namespace sa_search;
@@ -208,6 +238,7 @@ __global__ void k_gather_rows(const uint64_t *__restrict__ words, const uint32_t
 
 struct PresortLayout {
     size_t stats = 0, keys_in = 0, keys_out = 0, perm_in = 0, perm_out = 0, cub = 0, cub_bytes = 0, total = 0;
+    size_t defer_q = 0, defer_br = 0, defer_cnt = 0;  // SA_MATCH_DEFER: list of reads, their brackets, count
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -248,6 +279,15 @@ sa_status presort_layout(uint64_t Q, bool stats, bool presort, bool order_only, 
     }
     L.total = off;
     return SA_OK;
+}
+
+// the SA_MATCH_DEFER region after the rest of the workspace
+void defer_layout(uint64_t Q, PresortLayout &L) {
+    size_t off = L.total;
+    L.defer_q = off; off = align256(off + Q * 4);
+    L.defer_br = off; off = align256(off + Q * 8);
+    L.defer_cnt = off; off = align256(off + 4);
+    L.total = off;
 }
 
 constexpr uint32_t kDefaultKeyBases = 12;
@@ -517,6 +557,7 @@ extern "C" sa_status sa_match_workspace_size(const sa_index *idx, uint64_t Q, ui
     SA_CUDA_TRY(cudaSetDevice(idx->device));
     PresortLayout L;
     SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, flags & SA_MATCH_PRESORT, false, L));
+    if (flags & SA_MATCH_DEFER) defer_layout(Q, L);
     *bytes = L.total;
     return SA_OK;
 }
@@ -592,7 +633,9 @@ extern "C" sa_status sa_match_order(const sa_index *idx, const uint64_t *q_words
 
 static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, const uint32_t *q_len, uint32_t fixed_len,
                               uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *order,
-                              bool rows_ordered, cudaStream_t st, bool cooperative = false, uint32_t tree_flags = 0) {
+                              bool rows_ordered, cudaStream_t st, bool cooperative = false, uint32_t tree_flags = 0,
+                              uint32_t defer_big = 0, uint32_t *dq = nullptr, uint2 *dbr = nullptr,
+                              uint32_t *dcount = nullptr) {
     MatchArgs a;
     a.rows_ordered = rows_ordered;
 
@@ -657,6 +700,13 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
         if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
         return SA_OK;
     }
+    if (dq && !st_on && nw <= 4) {  // SA_MATCH_DEFER: light pass + deferred heavy reads
+        if (nw <= 1) e = launch_defer<1>(a, idx->layout, defer_big, dq, dbr, dcount, st);
+        else if (nw <= 2) e = launch_defer<2>(a, idx->layout, defer_big, dq, dbr, dcount, st);
+        else e = launch_defer<4>(a, idx->layout, defer_big, dq, dbr, dcount, st);
+        if (e != cudaSuccess) { sa_set_error("match launch: %s", cudaGetErrorString(e)); return SA_ECUDA; }
+        return SA_OK;
+    }
     // reads of more than 4 words: one thread per read, words from global memory; with
     // SA_MATCH_COOPERATIVE G = 8 / 16 / 32 lanes per read (measured slower)
     if (nw <= 1) e = launch_qw<1>(a, idx->layout, st_on, st);
@@ -691,8 +741,13 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
     if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED | SA_MATCH_COOPERATIVE | SA_MATCH_SMEM_TREE |
-                  0x1FF00u)) {
+                  0x1FF00u | SA_MATCH_DEFER | SA_MATCH_DEFER_LOG2(15))) {
         sa_set_error("unknown flags 0x%x", flags);
+        return SA_EINVAL;
+    }
+    const bool defer = (flags & SA_MATCH_DEFER) != 0;
+    if (defer && (flags & (SA_MATCH_ROWS_ORDERED | SA_MATCH_STATS | SA_MATCH_SMEM_TREE))) {
+        sa_set_error("SA_MATCH_DEFER does not combine with SA_MATCH_ROWS_ORDERED / SA_MATCH_STATS / SA_MATCH_SMEM_TREE");
         return SA_EINVAL;
     }
     if (Q == 0) return SA_OK;
@@ -700,6 +755,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
     const bool presort = (flags & SA_MATCH_PRESORT) && !order;
     PresortLayout L;
     SA_TRY(presort_layout(Q, flags & SA_MATCH_STATS, presort, false, L));
+    if (defer) defer_layout(Q, L);
     if (L.total > 0 && (!workspace || ws_bytes < L.total)) {
         sa_set_error("workspace too small: %zu < %zu bytes", ws_bytes, L.total);
         return SA_EINVAL;
@@ -717,8 +773,18 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         sa_set_error("SA_MATCH_ROWS_ORDERED needs the order the rows were arranged in");
         return SA_EINVAL;
     }
+    uint32_t big = 0, *dq = nullptr, *dcount = nullptr;
+    uint2 *dbr = nullptr;
+    if (defer) {
+        const uint32_t lg = (flags >> 18) & 15u;
+        big = 1u << (lg ? lg : 3u);
+        dq = reinterpret_cast<uint32_t *>(ws + L.defer_q);
+        dbr = reinterpret_cast<uint2 *>(ws + L.defer_br);
+        dcount = reinterpret_cast<uint32_t *>(ws + L.defer_cnt);
+    }
     return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st,
-                        (flags & SA_MATCH_COOPERATIVE) != 0, flags & (SA_MATCH_SMEM_TREE | 0x1FF00u));
+                        (flags & SA_MATCH_COOPERATIVE) != 0, flags & (SA_MATCH_SMEM_TREE | 0x1FF00u), big, dq, dbr,
+                        dcount);
 }
 
 // Synchronises the host pipeline's streams when sa_match_batch_host returns, on success and on every

@@ -906,6 +906,72 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     }
 }
 
+// ---- deferred heavy reads (SA_MATCH_DEFER) -----------------------------------------------------
+// The lanes of a warp search in lock step, so a warp takes as long as its slowest read: one read in a
+// repeat bucket (10-60 probes) holds 31 finished lanes.  Two passes instead: k_match_light does every read
+// whose k-mer bracket holds at most `big` suffixes (<= ~log2(big) + 2 probes) and appends the others --
+// read index and bracket -- to a list (one atomic per warp, lane order kept, so the list stays roughly in
+// key order); k_match_heavy then searches the listed reads with full warps, from the saved bracket.  The
+// same search (search_read / joint_search), the same results.
+template <int QW, int L>
+__global__ void SA_MATCH_BOUNDS k_match_light(const MatchArgs a, uint32_t big, uint32_t *__restrict__ dq,
+                                              uint2 *__restrict__ dbr, uint32_t *__restrict__ dcount) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.Q) return;
+    const unsigned act = __activemask();
+    uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;
+    const uint64_t row = a.rows_ordered ? t : q;
+    const uint32_t m = read_len(a, row);
+    QueryWords<QW> P;
+    load_read<QW>(a, row, m, P);
+    uint32_t lo, hi, steps = 0, texts = 0, ubytes = 0;
+    bool heavy = false;
+    uint32_t Lp1 = 0, R = 0;
+    if (m >= a.k && !a.big_sub && !a.tree_hash) {
+        const uint64_t x = P.first() >> (64 - 2 * a.k);
+        table_pair(a.table, x, Lp1, R);
+        Lp1 = min(max(Lp1, a.clo), a.chi);
+        R = min(max(R, a.clo), a.chi);
+        heavy = R - Lp1 > big;
+    }
+    const unsigned hv = __ballot_sync(act, heavy);
+    if (hv) {
+        const unsigned lane = threadIdx.x & 31, leader = (unsigned)(__ffs(act) - 1);
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(dcount, (uint32_t)__popc(hv));
+        base = __shfl_sync(act, base, (int)leader);
+        if (heavy) {
+            const uint32_t i = base + __popc(hv & ((1u << lane) - 1u));
+            dq[i] = (uint32_t)q;
+            dbr[i] = make_uint2(Lp1, R);
+            return;
+        }
+    }
+    if (m >= a.k && !a.big_sub && !a.tree_hash)
+        joint_search<L, false>(a, P, m, Lp1, R, 0, TreeLoc{0, 0}, 0, lo, hi, steps, texts, ubytes, nullptr);
+    else
+        search_read<L>(a, P, m, lo, hi, steps, texts, ubytes);
+    if (a.order) q = reload_u32(a.order + t);
+    reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+}
+
+// the listed reads (*dcount of them), grid-stride: slot i searches read dq[i] from bracket dbr[i]
+template <int QW, int L>
+__global__ void SA_MATCH_BOUNDS k_match_heavy(const MatchArgs a, const uint32_t *__restrict__ dq,
+                                              const uint2 *__restrict__ dbr, const uint32_t *__restrict__ dcount) {
+    const uint64_t cnt = *dcount;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = __ldg(dq + i);
+        const uint2 br = __ldg(dbr + i);
+        const uint32_t m = read_len(a, q);  // (rows_ordered is rejected with SA_MATCH_DEFER)
+        QueryWords<QW> P;
+        load_read<QW>(a, q, m, P);
+        uint32_t lo, hi, steps = 0, texts = 0, ubytes = 0;
+        joint_search<L, false>(a, P, m, br.x, br.y, 0, TreeLoc{0, 0}, 0, lo, hi, steps, texts, ubytes, nullptr);
+        reinterpret_cast<uint2 *>(a.out)[q] = make_uint2(lo, hi);
+    }
+}
+
 // k_match with the shared-memory top tree (north_star's "top levels of the SA
 // binary-search tree staged in shared memory via TMA"; the B200 form of the paper's shared-memory
 // tiles).  The reads are ordered (sa_match_order by key_bases bases), so a CTA's 256

@@ -634,3 +634,31 @@ def test_staged_long_read_verification(layout):
             bad = np.nonzero((got != want).any(axis=1))[0]
             assert bad.size == 0, f"offset {offset} presort {presort}: {bad.size} mismatches, q={bad[0]} m={lens[bad[0]]}"
     assert (want[:, 1] - want[:, 0] == 2).any()  # the duplication was exercised
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("defer", [1, 3, 6])
+def test_defer_heavy_reads_equal_oracle(layout, defer):
+    """SA_MATCH_DEFER: reads whose k-mer bracket holds more than 2^defer suffixes are searched in a second,
+    full-warp pass from their saved bracket.  Repeat-rich reference (big buckets), reads of 3-128 bases
+    (m < k: never deferred), the hazard batch, with and without an order, Q not a multiple of the warp;
+    every interval equals the oracle's."""
+    rng = random.Random(defer)
+    ref = synth.reference(synth.REF_REPEAT, 600_000, 81)
+    text = ref.tobytes().decode()
+    words, lens = synth.reads(ref, 20_003, 3, 128, 0.1, 0.05, 82)
+    hw, hl = synth.pack_strings(hazard_queries(text, 12, rng, extra=300) + ["A" * 60] * 100, stride=4)
+    words, lens = np.concatenate([words, hw]), np.concatenate([lens, hl])
+    S = oracle.encode(ref)
+    want = oracle.search_batch(S, oracle.sa_naive(S), words, lens).astype(np.uint32)
+    idx = sa.Index(ref, k=12, layout=layout)
+    w = torch.from_numpy(words.view(np.int64)).cuda()
+    l = torch.from_numpy(lens.view(np.int32)).cuda()
+    for order in (None, idx.order(w, l)):
+        got = idx.match(w, l, order=order, defer=defer)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy().view(np.uint32)
+        bad = np.nonzero((got != want).any(axis=1))[0]
+        assert bad.size == 0, f"{bad.size} mismatches, q={bad[0]} m={lens[bad[0]]}: {got[bad[0]]} vs {want[bad[0]]}"
+    with pytest.raises(sa.SAError):
+        idx.match(w, l, defer=3, want_stats=True)
