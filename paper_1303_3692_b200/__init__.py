@@ -346,8 +346,9 @@ class Index:
             if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_DEFER) else 0
         if need and (workspace is None or workspace.numel() < need):
             workspace = _empty(need, torch.uint8, words.device, stream)
+        ws_ptr, ws_bytes = (_dptr(workspace), workspace.numel()) if workspace is not None else (None, 0)
         _check(lib().sa_match_batch(self._h, _dptr(words), _dptr(lens), int(fixed_len or 0), stride, Q, _dptr(order),
-                                    _dptr(out), _dptr(workspace) if need else None, need, flags, _stream_ptr(stream)),
+                                    _dptr(out), ws_ptr, ws_bytes, flags, _stream_ptr(stream)),
                "sa_match_batch")
         if want_stats:  # [2, Q]: row 0 steps | text windows << 16, row 1 algorithmic bytes (include/sa.h)
             return out, workspace[: 8 * Q].view(torch.int32).view(2, Q)
