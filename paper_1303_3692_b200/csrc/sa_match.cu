@@ -207,12 +207,7 @@ __global__ void k_presort_keys(const uint64_t *__restrict__ words, const uint32_
             m = min(lens ? __ldg(lens + q) : fixed_len, 32u * stride);
             w0 = __ldg(reinterpret_cast<const unsigned long long *>(words + q * stride));
         }
-#ifdef SA_SORTED_KEYS  // the first 16 bases (masked to the read's length); the sort uses the top 2*key_bases bits
-        const uint32_t pre = short_last ? (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases))
-                                        : (uint32_t)((w0 & prefix_mask(min(m, 16u))) >> 32);
-#else
         const uint32_t pre = (uint32_t)((w0 & prefix_mask(min(m, key_bases))) >> (64 - 2 * key_bases));
-#endif
         const uint32_t key = (short_last && m < key_bases) ? (1u << (2 * key_bases)) : pre;
         if (k64) {  // (SA_ORDER_PACKED)
             k64[q] = ((uint64_t)key << 27) | q;
@@ -342,13 +337,6 @@ sa_status order_reads(const uint64_t *q_words, const uint32_t *q_len, uint32_t f
     k_presort_keys<<<(unsigned)blocks, 256, 0, st>>>(q_words, q_len, fixed_len, stride, dense_words, Q, key_bases,
                                                      short_last, keys_in, perm_in, nullptr);
     SA_CUDA_TRY(cudaGetLastError());
-#ifdef SA_SORTED_KEYS  // keys_out: the reads' 16-base keys in slot order (k_match reads them: sorted_keys_of)
-    if (!short_last) {
-        SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q,
-                                                    32 - 2 * (int)key_bases, 32, st));
-        return SA_OK;
-    }
-#endif
     SA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ws + L.cub, b, keys_in, keys_out, perm_in, order, (int64_t)Q, 0,
                                                 end_bit, st));
     return SA_OK;
@@ -647,9 +635,8 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
                               uint32_t stride, uint64_t Q, uint32_t *out, uint32_t *stats, const uint32_t *order,
                               bool rows_ordered, cudaStream_t st, bool cooperative = false, uint32_t tree_flags = 0,
                               uint32_t defer_big = 0, uint32_t *dq = nullptr, uint2 *dbr = nullptr,
-                              uint32_t *dcount = nullptr, const uint32_t *skeys = nullptr) {
+                              uint32_t *dcount = nullptr) {
     MatchArgs a;
-    a.skeys = skeys;
     a.rows_ordered = rows_ordered;
 
     a.text = idx->text;
@@ -795,17 +782,9 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         dbr = reinterpret_cast<uint2 *>(ws + L.defer_br);
         dcount = reinterpret_cast<uint32_t *>(ws + L.defer_cnt);
     }
-    const uint32_t *skeys = nullptr;
-#ifdef SA_SORTED_KEYS  // experiment: the workspace of the sa_match_order call that made `order` holds its sorted keys
-    if (order && !presort && !stats && !rows_ordered && workspace) {
-        PresortLayout OL;
-        SA_TRY(presort_layout(Q, false, true, true, OL));
-        if (ws_bytes >= OL.keys_out + Q * 4) skeys = reinterpret_cast<const uint32_t *>(ws + OL.keys_out);
-    }
-#endif
     return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st,
                         (flags & SA_MATCH_COOPERATIVE) != 0, flags & (SA_MATCH_SMEM_TREE | 0x1FF00u), big, dq, dbr,
-                        dcount, skeys);
+                        dcount);
 }
 
 // Synchronises the host pipeline's streams when sa_match_batch_host returns, on success and on every

@@ -52,7 +52,6 @@ struct MatchArgs {
     const unsigned long long *__restrict__ tree_hash;  // SA_INDEX_BUCKET_TREE: x << 32 | first line, empty = ~0
     const uint4 *__restrict__ tree;                     // its lines (4 records of 32 bytes, 3 used)
     uint32_t tree_bits;
-    const uint32_t *__restrict__ skeys;  // SA_SORTED_KEYS build: slot t's read starts with the 16 bases skeys[t]
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -720,8 +719,7 @@ __device__ __forceinline__ void joint_search(const MatchArgs &a, const RD &P, ui
 template <int L, bool TREE = false, bool BT = false, class RD>
 __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uint32_t m, uint32_t &lo,
                                             uint32_t &hi, uint32_t &steps, uint32_t &texts, uint32_t &ubytes,
-                                            const TreeCtx *tc = nullptr, uint32_t *split_sa = nullptr,
-                                            const uint2 *pre = nullptr) {
+                                            const TreeCtx *tc = nullptr, uint32_t *split_sa = nullptr) {
     const uint32_t k = a.k;
     auto clamp = [&](uint32_t v) { return min(max(v, a.clo), a.chi); };
     if (m == 0) {  // the empty read is a prefix of every suffix (reading A12): [0, n), clamped
@@ -747,8 +745,7 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
     // all suffixes before T[x] are < P, all from T[x+1] on are > P
     const uint64_t x = P.first() >> (64 - 2 * k);
     uint32_t Lp1, R;
-    if (pre) { Lp1 = pre->x; R = pre->y; }  // (loaded from the sorted key, in parallel with the read's row)
-    else table_pair(a.table, x, Lp1, R);
+    table_pair(a.table, x, Lp1, R);
     Lp1 = clamp(Lp1);
     R = clamp(R);
     ubytes += 8;  // T[x], T[x+1]
@@ -866,13 +863,6 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
     if (t >= a.Q) return;
     uint64_t q = a.order ? (uint64_t)__ldg(a.order + t) : t;  // the read; its result goes to out[q]
     const uint64_t row = a.rows_ordered ? t : q;               // where its bases are
-#ifdef SA_SORTED_KEYS
-    // the bracket from the ordering's sorted key (coalesced), issued before the row gather it no longer
-    // waits for; used when the read has >= k bases (the key is then its first k bases)
-    uint2 pb = make_uint2(0, 0);
-    const bool have_pre = QW > 0 && a.skeys != nullptr && !a.route;
-    if (have_pre) table_pair(a.table, (uint64_t)(__ldg(a.skeys + t) >> (32 - 2 * a.k)), pb.x, pb.y);
-#endif
     const uint32_t m = read_len(a, row);
     QueryWords<QW> P;
     load_read<QW>(a, row, m, P);
@@ -898,13 +888,6 @@ __global__ void SA_MATCH_BOUNDS k_match(const MatchArgs a) {
             else hi = lo;
         }
     } else {
-#ifdef SA_SORTED_KEYS
-        if (have_pre && m >= a.k) {
-            pb.x = min(max(pb.x, a.clo), a.chi);
-            pb.y = min(max(pb.y, a.clo), a.chi);
-            search_read<L, false, BT>(a, P, m, lo, hi, steps, texts, ubytes, nullptr, nullptr, &pb);
-        } else
-#endif
         search_read<L, false, BT>(a, P, m, lo, hi, steps, texts, ubytes);
     }
     // Alg. 1 lines 44-45: res[thd<<1] = LB, res[(thd<<1)+1] = RB (reading A8), half-open here.
