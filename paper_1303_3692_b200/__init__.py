@@ -30,6 +30,7 @@ SA_MATCH_COOPERATIVE = 32   # sa_match_batch flags: reads over 128 bases searche
 SA_MATCH_SMEM_TREE = 64     # sa_match_batch flags: shared-memory top tree per CTA (needs an order)
 SA_ORDER_BUCKETS = 0x100    # sa_match_order key_bases flag: bucket placement (not stable), for L2-sized batches
 SA_MATCH_DEFER = 1 << 17    # sa_match_batch flags: reads in big k-mer buckets deferred to a second full-warp pass
+SA_MATCH_WIDE = 1 << 24     # sa_match_batch flags: the large-batch load hints at any batch size
 SA_INDEX_BUILD_DC3 = 4      # sa_index_opts.flags: build the SA with DC3 (the paper's algorithm)
 SA_INDEX_SUBTABLE = 8       # sa_index_opts.flags: (k+4)-base sub-tables for buckets of > 32 suffixes
 SA_INDEX_BUCKET_TREE = 16   # sa_index_opts.flags: line-packed binary-search trees for buckets of >= 32 suffixes
@@ -308,7 +309,7 @@ class Index:
     def match(self, words, lens=None, fixed_len: Optional[int] = None, out=None, stream=None, want_stats=False,
               presort: bool = False, workspace=None, order=None, rows_ordered: bool = False,
               n_reads: Optional[int] = None, cooperative: bool = False, smem_tree: int = 0, tree_key_bases: int = 0,
-              defer: int = 0):
+              defer: int = 0, wide: bool = False):
         """sa_match_batch on device tensors.
 
         words: CUDA int64 tensor [Q, stride] (uint64 bit patterns, include/sa.h layout).
@@ -321,6 +322,7 @@ class Index:
         smem_tree: L > 0 selects SA_MATCH_SMEM_TREE with L levels (tree_key_bases: the order's key length).
         defer: b > 0 selects SA_MATCH_DEFER: reads whose k-mer bracket holds more than 2^b suffixes go to a
         second pass.
+        wide: SA_MATCH_WIDE (the large-batch load hints, automatic from 2^24 reads, at any batch size).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [2, Q]: row 0 steps | text windows << 16, row 1 the
@@ -342,6 +344,8 @@ class Index:
             flags |= SA_MATCH_SMEM_TREE | ((int(smem_tree) & 15) << 8) | ((int(tree_key_bases) & 31) << 12)
         if defer:
             flags |= SA_MATCH_DEFER | ((int(defer) & 15) << 18)
+        if wide:
+            flags |= SA_MATCH_WIDE
         need = self.workspace_size(Q, stride, flags) \
             if flags & (SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_DEFER) else 0
         if need and (workspace is None or workspace.numel() < need):

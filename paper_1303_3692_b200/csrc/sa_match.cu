@@ -664,6 +664,11 @@ static sa_status match_launch(const sa_index *idx, const uint64_t *q_words, cons
     a.chi = (uint32_t)idx->n;
     a.route = nullptr;
     a.route_bases = 0;
+#ifndef SA_NO_WIDE  // (A/B build: never wide)
+    a.wide = Q >= kWideQ || (tree_flags & SA_MATCH_WIDE);
+#else
+    a.wide = false;
+#endif
     if (idx->nparts > 1) {
         // a partition holds table entries [x_base, x_base + table_entries) and SA ranks [rank_base, rank_end):
         // address them with their global indices through shifted base pointers; every bracket is clamped
@@ -741,7 +746,7 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
     sa_clear_error();
     SA_TRY(check_match_args(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi));
     if (flags & ~(SA_MATCH_STATS | SA_MATCH_PRESORT | SA_MATCH_ROWS_ORDERED | SA_MATCH_COOPERATIVE | SA_MATCH_SMEM_TREE |
-                  0x1FF00u | SA_MATCH_DEFER | SA_MATCH_DEFER_LOG2(15))) {
+                  0x1FF00u | SA_MATCH_DEFER | SA_MATCH_DEFER_LOG2(15) | SA_MATCH_WIDE)) {
         sa_set_error("unknown flags 0x%x", flags);
         return SA_EINVAL;
     }
@@ -783,7 +788,8 @@ extern "C" sa_status sa_match_batch(const sa_index *idx, const uint64_t *q_words
         dcount = reinterpret_cast<uint32_t *>(ws + L.defer_cnt);
     }
     return match_launch(idx, q_words, q_len, fixed_len, stride_words, Q, out_lohi, stats, order, rows_ordered, st,
-                        (flags & SA_MATCH_COOPERATIVE) != 0, flags & (SA_MATCH_SMEM_TREE | 0x1FF00u), big, dq, dbr,
+                        (flags & SA_MATCH_COOPERATIVE) != 0, flags & (SA_MATCH_SMEM_TREE | 0x1FF00u | SA_MATCH_WIDE), big,
+                        dq, dbr,
                         dcount);
 }
 

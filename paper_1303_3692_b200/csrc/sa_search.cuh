@@ -52,6 +52,7 @@ struct MatchArgs {
     const unsigned long long *__restrict__ tree_hash;  // SA_INDEX_BUCKET_TREE: x << 32 | first line, empty = ~0
     const uint4 *__restrict__ tree;                     // its lines (4 records of 32 bytes, 3 used)
     uint32_t tree_bits;
+    bool wide;  // a large batch (>= kWideQ reads): 64-byte L2 fetches for the read row and the table pair
 };
 
 // ---- the read ---------------------------------------------------------------------------------
@@ -64,15 +65,15 @@ struct QueryWords {
     uint64_t w[QW];
     // the whole read row in one vector load (one request, one sector) when the stride equals QW:
     // 256-bit (LDG.E.ENL2.256) for 4 words, 128-bit for 2; rows are then 32- / 16-byte aligned
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw, bool vec) {
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ p, uint32_t nw, bool vec, bool wide = false) {
         if constexpr (QW == 4) {
             if (vec) {
-                ld_v4u64(p, w[0], w[1], w[2], w[3]);
+                ld_row_v4u64(p, wide, w[0], w[1], w[2], w[3]);
                 return;
             }
         } else if constexpr (QW == 2) {
             if (vec) {
-                ld_v2u64(p, w[0], w[1]);
+                ld_row_v2u64(p, wide, w[0], w[1]);
                 return;
             }
         }
@@ -115,7 +116,7 @@ struct QueryWords<0> {
 #pragma unroll
         for (int j = 0; j < kHead; ++j) h[j] = gword((uint32_t)j);
     }
-    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool v) {
+    __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool v, bool = false) {
         p = q;
         nw = n;
         vec = v;
@@ -350,8 +351,9 @@ struct Rec {
 };
 
 // T[x] and T[x+1]: one aligned 16-byte load unless x sits in the last slot of its 16-byte group.
-__device__ __forceinline__ void table_pair(const uint32_t *__restrict__ T, uint64_t x, uint32_t &a, uint32_t &b) {
-    const uint4 v = ld_v4u32(T + (x & ~3ull));
+__device__ __forceinline__ void table_pair(const uint32_t *__restrict__ T, uint64_t x, uint32_t &a, uint32_t &b,
+                                           bool wide = false) {
+    const uint4 v = ld_tab_v4u32(T + (x & ~3ull), wide);
     switch (x & 3) {
     case 0: a = v.x; b = v.y; break;
     case 1: a = v.y; b = v.z; break;
@@ -745,7 +747,7 @@ __device__ __forceinline__ void search_read(const MatchArgs &a, const RD &P, uin
     // all suffixes before T[x] are < P, all from T[x+1] on are > P
     const uint64_t x = P.first() >> (64 - 2 * k);
     uint32_t Lp1, R;
-    table_pair(a.table, x, Lp1, R);
+    table_pair(a.table, x, Lp1, R, a.wide);
     Lp1 = clamp(Lp1);
     R = clamp(R);
     ubytes += 8;  // T[x], T[x+1]
@@ -834,7 +836,7 @@ __device__ __forceinline__ uint32_t read_len(const MatchArgs &a, uint64_t q) {
 template <int QW>
 __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint32_t m, QueryWords<QW> &P) {
     if (a.stride == 0) P.load_dense(a.words, 2ull * m * row, (m + 31) >> 5, a.dense_words);
-    else P.load(a.words + row * a.stride, (m + 31) >> 5, a.vec_rows);
+    else P.load(a.words + row * a.stride, (m + 31) >> 5, a.vec_rows, a.wide);
 }
 
 // One read per thread slot, all lanes of a warp in lock step (with sa_match_order the lanes hold

@@ -662,3 +662,23 @@ def test_defer_heavy_reads_equal_oracle(layout, defer):
         assert bad.size == 0, f"{bad.size} mismatches, q={bad[0]} m={lens[bad[0]]}: {got[bad[0]]} vs {want[bad[0]]}"
     with pytest.raises(sa.SAError):
         idx.match(w, l, defer=3, want_stats=True)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_wide_batch_loads_equal_oracle(layout):
+    """SA_MATCH_WIDE: the large-batch load hints (L2::64B for the read row and the table pair; automatic from
+    2^25 reads) forced on a small batch: every interval equals the oracle's, strided rows of 1 / 2 / 4 words
+    (the 128- and 256-bit row loads) and long reads, with and without an order."""
+    ref = synth.reference(synth.REF_REPEAT, 700_000, 85)
+    S = oracle.encode(ref)
+    sa_ref = oracle.sa_naive(S)
+    idx = sa.Index(ref, layout=layout)
+    for m_lo, m_hi in [(5, 32), (33, 64), (65, 128), (100, 100), (129, 300)]:
+        words, lens = synth.reads(ref, 20_000, m_lo, m_hi, 0.1, 0.05, 86 + m_hi)
+        want = oracle.search_batch(S, sa_ref, words, lens).astype(np.uint32)
+        w = torch.from_numpy(words.view(np.int64)).cuda()
+        l = torch.from_numpy(lens.view(np.int32)).cuda()
+        for order in (None, idx.order(w, l)):
+            got = idx.match(w, l, order=order, wide=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), want), (m_lo, m_hi, order is None)
