@@ -222,6 +222,12 @@ __device__ __forceinline__ void ld_row_v2u64(const void *p, bool wide, uint64_t 
     if (wide) asm("ld.global.nc.L1::no_allocate.L2::64B.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
     else asm(SA_LD_OP ".v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
 }
+__device__ __forceinline__ uint64_t ld_row_u64(const uint64_t *p, bool wide) {
+    uint64_t v;
+    if (wide) asm("ld.global.nc.L1::no_allocate.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    else asm(SA_LD_OP ".u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint4 ld_tab_v4u32(const void *p, bool wide) {
     uint4 v;
     if (wide) asm("ld.global.nc.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));

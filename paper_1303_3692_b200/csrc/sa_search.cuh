@@ -79,7 +79,7 @@ struct QueryWords {
         }
 #pragma unroll
         for (int j = 0; j < QW; ++j)
-            w[j] = (j < (int)nw) ? ld_u64(p + j) : 0ull;
+            w[j] = (j < (int)nw) ? ld_row_u64(p + j, wide) : 0ull;
     }
     // dense layout: the read starts at bit `bit` of a continuous stream of `total` words
     __device__ __forceinline__ void load_dense(const uint64_t *__restrict__ s, uint64_t bit, uint32_t nw,
@@ -116,6 +116,9 @@ struct QueryWords<0> {
 #pragma unroll
         for (int j = 0; j < kHead; ++j) h[j] = gword((uint32_t)j);
     }
+    // (the large-batch row hint of QueryWords<QW> is not used here: L1::no_allocate.L2::64B on the row
+    // words of 150-250-base reads measured 9.90 / 10.37 vs 8.24 / 8.55 ms per 50 M reads -- their words
+    // are read more than once -- profiles/r02/r02ai)
     __device__ __forceinline__ void load(const uint64_t *__restrict__ q, uint32_t n, bool v, bool = false) {
         p = q;
         nw = n;
