@@ -691,7 +691,8 @@ def main():
                       "frac": kernel_qps / ceiling,
                       "note": "ceiling = every access an independent random access; frac > 1 is the line sharing "
                               "the read ordering buys (neighbouring reads touch the same table / record lines); "
-                              "line_frac = DRAM line rate of k_match (ncu traffic) / (R_rand x 128 B)"}
+                              "line_frac = DRAM line rate of k_match (ncu traffic) / (R_rand x 128 B); with the 64-B "
+                              "row / table fetches of large batches a lower bound on its access rate"}
                 if line["roofline"].get("traffic_GBps"):
                     rr["dram_line_GBps"] = line["roofline"]["traffic_GBps"]
                     rr["line_frac"] = line["roofline"]["traffic_GBps"] / (rg["Gaccess_per_s"] * 128.0)
