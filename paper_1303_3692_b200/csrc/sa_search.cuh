@@ -849,7 +849,11 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 // prefetches the next read's row during the current search (profiles/r01t: 2% slower -- the kernel is
 // bound by DRAM line throughput, not by the latency of the chain's head).
 #ifndef SA_MATCH_THREADS
-#define SA_MATCH_THREADS 256  // block size of k_match (A/B builds: variants/)
+// block size of k_match (A/B builds: variants/).  64: a block retires as soon as its two warps finish, so a
+// slow (repeat or long) read holds 64 thread slots instead of 256 -- k_match 9.97 vs 10.05 ms per 100 M
+// reads, 1.40 vs 1.47 per 12.5 M, 2.68 vs 2.80 per 25 M, C5 m = 150 / 500 7.45 / 10.22 vs 8.16 / 10.79 per
+// 50 M (profiles/r02/r02am, r02an; round 1's kernel had measured flat, profiles/r01-3/e_*)
+#define SA_MATCH_THREADS 64
 #endif
 // minimum resident blocks per SM requested from ptxas (a register cap): 5 x 256 threads = 62.5%
 // occupancy = at most 48 registers, the plateau measured in r01-3 (profiles/r01-3/e_*: 40 registers
