@@ -1,5 +1,5 @@
 # final HEAD verification of round 2 (64-thread k_match blocks): GPU tests (incl. the full-size slow tier), smoke,
-# the 2/4/8-GPU per-rank batches, the C5 sweep), launch lists + ncu --set full of k_match (C4, C5 m=1000)
+# bench lines (C4, C4 at the 2/4/8-GPU per-rank batches, the C5 sweep), launch lists + ncu --set full of k_match (C4, C5 m=1000)
 out=gpurun_out/r02ao; mkdir -p $out
 nvidia-smi > $out/nvidia-smi.txt 2>&1
 timeout 1800 python -m pytest tests -m "gpu and not slow" -x -q > $out/pytest_gpu.txt 2>&1; echo "rc=$?" >> $out/pytest_gpu.txt
