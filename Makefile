@@ -34,10 +34,11 @@ $(shell mkdir -p build)
 # --libs): sa_match.cu (the search kernels) recompiled with the defines, linked with the default objects
 VARIANTS := ldcg ldnoalloc ldca l2_64 l2_64na t128 t64 t128_m12 t64_m32 t256_m6 t64_m24 t128_m10 t64_m20 \
             t256_m1 outpad t256_m5 head1 head2 head3 head1_m5 bulkpf chunk2m3 m3 longwarp dual dual3 hostnoorder \
-            packed onesweep staged stagedwarp nowide t32_m32 t96_m13 t256_m5b
+            packed onesweep staged stagedwarp nowide t32_m32 t96_m13 t256_m5b allwide
 DEFS_onesweep := -DSA_ORDER_ONESWEEP
 DEFS_staged := -DSA_MATCH_STAGED
 DEFS_nowide := -DSA_NO_WIDE
+DEFS_allwide := -DSA_WIDE_Q_LOG2=0
 DEFS_t32_m32 := -DSA_MATCH_THREADS=32 -DSA_MATCH_MINB=32
 DEFS_t96_m13 := -DSA_MATCH_THREADS=96 -DSA_MATCH_MINB=13
 DEFS_t256_m5b := -DSA_MATCH_THREADS=256 -DSA_MATCH_MINB=5

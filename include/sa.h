@@ -126,7 +126,7 @@ typedef struct {
  * SA_MATCH_ROWS_ORDERED, SA_MATCH_STATS or SA_MATCH_SMEM_TREE. */
 #define SA_MATCH_DEFER (1u << 17)
 /* sa_match_batch flag: the large-batch load hints (a 64-byte L2 fetch for the read row and the bracket
- * table pair; automatic from 2^24 reads per call) at any batch size.  Same results. */
+ * table pair; automatic from 2^20 reads per call) at any batch size.  Same results. */
 #define SA_MATCH_WIDE (1u << 24)
 #define SA_MATCH_DEFER_LOG2(b) (((uint32_t)(b) & 15u) << 18)
 #define SA_MATCH_TREE_LEVELS(l) (((uint32_t)(l) & 15u) << 8)

@@ -322,7 +322,7 @@ class Index:
         smem_tree: L > 0 selects SA_MATCH_SMEM_TREE with L levels (tree_key_bases: the order's key length).
         defer: b > 0 selects SA_MATCH_DEFER: reads whose k-mer bracket holds more than 2^b suffixes go to a
         second pass.
-        wide: SA_MATCH_WIDE (the large-batch load hints, automatic from 2^24 reads, at any batch size).
+        wide: SA_MATCH_WIDE (the large-batch load hints, automatic from 2^20 reads, at any batch size).
         workspace: optional CUDA uint8 tensor of >= workspace_size() bytes (allocated if None).
         Returns a CUDA int32 tensor [Q, 2] holding uint32 (lo, hi) -- view it as uint32 on the host --
         and, with want_stats, also an int32 tensor [2, Q]: row 0 steps | text windows << 16, row 1 the

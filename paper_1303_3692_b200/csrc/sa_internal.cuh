@@ -209,9 +209,10 @@ __device__ __forceinline__ void ld_v4u64(const void *p, uint64_t &a, uint64_t &b
 
 // Large batches (MatchArgs::wide, >= kWideQ reads): the read row (one random 32-byte row per read, used
 // once) is loaded with L1::no_allocate + an L2::64B fetch (half the DRAM bytes of a 128-byte line), and
-// the bracket-table pair with an L2::64B fetch.  Measured (profiles/r02/r02ae, r02af): k_match 10.05 vs
-// 10.45 ms per 100 M reads, but 1.49-1.50 vs 1.47 ms per 12.5 M (fewer ordered neighbours share the 128-B
-// lines), so small batches keep the plain loads.  A warp-uniform branch selects the instruction.
+// the bracket-table pair with an L2::64B fetch.  Measured (profiles/r02/r02ae, r02af, r02aq): k_match 10.05 vs
+// 10.45 ms per 100 M reads; at 12.5 M 1.49-1.50 vs 1.47 ms with 256-thread blocks, 1.351 vs 1.363 with the
+// 64-thread blocks.  Batches below 2^20 reads (L2-sized indexes and batches) keep the plain loads.  A
+// warp-uniform branch selects the instruction.
 __device__ __forceinline__ void ld_row_v4u64(const void *p, bool wide, uint64_t &a, uint64_t &b, uint64_t &c,
                                              uint64_t &d) {
     if (wide) asm("ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0, %1, %2, %3}, [%4];"
@@ -234,7 +235,10 @@ __device__ __forceinline__ uint4 ld_tab_v4u32(const void *p, bool wide) {
     else asm(SA_LD_OP ".v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
-constexpr uint64_t kWideQ = 1ull << 24;  // reads per launch from which MatchArgs::wide is set (16.8 M)
+#ifndef SA_WIDE_Q_LOG2
+#define SA_WIDE_Q_LOG2 20
+#endif
+constexpr uint64_t kWideQ = 1ull << SA_WIDE_Q_LOG2;  // reads per launch from which MatchArgs::wide is set (1 M)
 
 // a load the compiler may not merge with an earlier load of the same address (re-reads a value instead
 // of keeping it live in a register)

@@ -667,7 +667,7 @@ def test_defer_heavy_reads_equal_oracle(layout, defer):
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_wide_batch_loads_equal_oracle(layout):
     """SA_MATCH_WIDE: the large-batch load hints (L2::64B for the read row and the table pair; automatic from
-    2^24 reads) forced on a small batch: every interval equals the oracle's, strided rows of 1 / 2 / 4 words
+    2^20 reads) forced on a small batch: every interval equals the oracle's, strided rows of 1 / 2 / 4 words
     (the 128- and 256-bit row loads) and long reads, with and without an order."""
     ref = synth.reference(synth.REF_REPEAT, 700_000, 85)
     S = oracle.encode(ref)
