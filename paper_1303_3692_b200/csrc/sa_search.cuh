@@ -855,13 +855,13 @@ __device__ __forceinline__ void load_read(const MatchArgs &a, uint64_t row, uint
 // 50 M (profiles/r02/r02am, r02an; round 1's kernel had measured flat, profiles/r01-3/e_*)
 #define SA_MATCH_THREADS 64
 #endif
-// minimum resident blocks per SM requested from ptxas (a register cap): 5 x 256 threads = 62.5%
-// occupancy = at most 48 registers, the plateau measured in r01-3 (profiles/r01-3/e_*: 40 registers
-// spill and run slower, 64 registers (50%) run 9% slower)
+// minimum resident blocks per SM requested from ptxas (a register cap): 1280 threads per SM (20 x 64) =
+// 62.5% occupancy = at most 48 registers, the plateau measured in r01-3 (profiles/r01-3/e_*: 40 registers
+// spill and run slower, 64 registers (50%) run 9% slower; again with 64-thread blocks, profiles/r02/r02ap)
 #ifndef SA_MATCH_MINB
 #define SA_MATCH_MINB (1280 / SA_MATCH_THREADS)
 #endif
-// (the long-read instantiation, QW = 0: 4 x 256 threads = 64 registers, the r01 build's allocation)
+// (the long-read instantiation, QW = 0: 1024 threads per SM = 64 registers, the r01 build's allocation)
 #ifndef SA_MATCH_MINB_LONG
 #define SA_MATCH_MINB_LONG (1024 / SA_MATCH_THREADS)
 #endif
